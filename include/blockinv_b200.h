@@ -1,0 +1,155 @@
+/*
+ * blockinv_b200.h -- C ABI of the B200 (sm_100a) blockwise-inversion library
+ * (libblockinv_b200.so).  The drop-in boundary for the reference `blockinv`
+ * hot path (/root/reference/pkg/src/blockinv).
+ *
+ * Conventions
+ *  - Plain C types only: pointers, 64-bit sizes, int status.  No torch types.
+ *  - Every matrix pointer is a DEVICE pointer to row-major (C-order) float64
+ *    with an explicit leading dimension `ld` (elements, >= cols).  The
+ *    library never frees caller memory; callers size and own every buffer,
+ *    including workspaces (query functions give the byte counts).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Return value: BI_OK (0) or one of the BI_E* codes; bi_last_error()
+ *    returns a thread-local message for the last failure.
+ *  - Singular pivots are not an error of the call: they are reported through
+ *    `info` arrays / out-parameters exactly where the reference raises
+ *    SingularBlock / SingularMatrix (errors.py:17-38).
+ */
+#ifndef BLOCKINV_B200_H
+#define BLOCKINV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BI_OK = 0,
+  BI_ESINGULAR = 1, /* a pivot block / Schur complement is singular      */
+  BI_EDIM = 2,      /* shape / argument error (DimensionMismatch, ...)    */
+  BI_ECUDA = 3,     /* CUDA runtime error                                 */
+  BI_ENCCL = 4,     /* collective error (reserved: multi-GPU scheduler)   */
+  BI_EUNSUPPORTED = 5
+};
+
+/* Library identity and the last error message of the calling thread. */
+int bi_version(void);
+const char* bi_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * K1: FP64 DMMA GEMM.  D = [Cin] + (alpha_sign)*A*B, strided batched.
+ * Replaces core._mm_acc / multiply / schur_accumulate
+ * (core.py:115-139, 142-170, 173-192) and engine.fox_block_multiply
+ * (engine.py:202-249): out = (+-1)*a@b, or out += ... when accumulating.
+ * Cin may be NULL (beta = 0) and may equal D (in-place accumulate, the
+ * `accumulate=True` form).  A/B must not alias D (core.py:161-163).
+ * ---------------------------------------------------------------------- */
+int bi_gemm(int64_t m, int64_t n, int64_t k, int alpha_sign,
+            const double* a, int64_t lda, int64_t stride_a,
+            const double* b, int64_t ldb, int64_t stride_b,
+            const double* cin, int64_t ldc, int64_t stride_c,
+            double* d, int64_t ldd, int64_t stride_d,
+            int batch, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K2/K3: batched in-place-style Gauss-Jordan inversion with partial pivoting
+ * (pivot tolerance 1e-12 * n * max|block|, as gauss_jordan_oracle,
+ * core.py:379-402).  Inverts `count` n x n blocks:
+ *   out[i] = inverse(in[i]),  in[i] = in + i*stride_in (ld_in),
+ *   out[i] = out + i*stride_out (ld_out).
+ * Replaces core.invert_small (core.py:350-376), the engine's leaf inverter
+ * engine._leaf_invert (engine.py:449-457) and the `invert_sub(block, out)`
+ * plugin protocol (schur.py:16-18, 104-111).  info[i] = 0 on success, or
+ * c+1 where c is the first pivot column with no usable pivot.
+ * `workspace` must hold bi_inv_workspace_bytes(count, n) bytes.
+ * ---------------------------------------------------------------------- */
+int64_t bi_inv_workspace_bytes(int count, int64_t n);
+int bi_inv_batched(int count, int64_t n,
+                   const double* in, int64_t ld_in, int64_t stride_in,
+                   double* out, int64_t ld_out, int64_t stride_out,
+                   int* info, void* workspace, int64_t workspace_bytes,
+                   void* stream);
+
+/* ------------------------------------------------------------------------
+ * Step engine: run_inversion (engine.py:482-542) over `batch` independent
+ * matrices that share one partition `sizes[nblocks]` (nblocks a power of 2,
+ * partition.py:87-99).  Executes stepids [first_step, last_step] of the
+ * 2*nblocks-1 step schedule (engine.py:73-162); `last_step` < N_s is the
+ * `stop_after_step` form.  M_inv is written in place (zero-filled by the
+ * caller before step 1, storage.py:391-411).
+ *
+ *   bi_engine_create   -> opaque plan; validates sizes (InvalidOrder).
+ *   bi_engine_workspace_bytes -> device workspace (T-sets, leaf scratch,
+ *                          descriptor tables) the caller must provide.
+ *   bi_engine_bind     -> binds device buffers and uploads the schedule.
+ *   bi_engine_run      -> enqueues steps on `stream` (graph-captured when
+ *                          use_graph != 0); asynchronous.
+ *   bi_engine_status   -> synchronizes; reports the first singular leaf as
+ *                          (step, quad, matrix) like SingularBlock(step,quad)
+ *                          (engine.py:320-328); returns BI_ESINGULAR then.
+ *   bi_engine_counters -> OpCounters semantics of the executed steps
+ *                          (engine.py:317, 344-345, 411):
+ *                          out[0]=multiplies out[1]=inversions out[2]=reductions
+ *                          out[3]=gemm flops (algorithmic) out[4]=leaf flops.
+ * ---------------------------------------------------------------------- */
+typedef struct bi_engine bi_engine;
+int bi_engine_create(bi_engine** out, int nblocks, const int64_t* sizes, int batch);
+int64_t bi_engine_workspace_bytes(const bi_engine* e);
+int bi_engine_bind(bi_engine* e,
+                   const double* m, int64_t ldm, int64_t stride_m,
+                   double* minv, int64_t ldi, int64_t stride_i,
+                   void* workspace, int64_t workspace_bytes, void* stream);
+int bi_engine_run(bi_engine* e, int first_step, int last_step, int use_graph, void* stream);
+int bi_engine_status(bi_engine* e, int* fail_step, int* fail_quad, int* fail_matrix);
+int bi_engine_counters(const bi_engine* e, int first_step, int last_step, double out[5]);
+/* T-set access for step-state parity: pointer + ld of the level-`level`
+ * provisional square of quad `quad` of matrix `matrix` (S_D at A's
+ * position, R at B's, L at C's, S_A at D's; storage.py:166-262). */
+int bi_engine_tset_square(const bi_engine* e, int level, int quad, int matrix,
+                          double** ptr, int64_t* ld, int64_t* side);
+int bi_engine_destroy(bi_engine* e);
+
+/* ------------------------------------------------------------------------
+ * Single-level 2x2 pivot formulas on one square matrix m (order n, split p).
+ * pivot = 'A' : invert_via_a (schur.py:114-139, Eq. 2)
+ * pivot = 'D' : invert_via_d (schur.py:142-164, Eq. 3; the singular-A11 path)
+ * pivot = 'X' : invert_via_ad (schur.py:219-259, Eq. 7)
+ * Sub-inversions use K3.  On a singular pivot returns BI_ESINGULAR with
+ * *fail_block = 'A','D','a' (SchurA) or 'd' (SchurD) -- the labels of
+ * schur._sub_inverse (schur.py:104-111).  out (n x n) must not alias m.
+ * ---------------------------------------------------------------------- */
+int64_t bi_schur2x2_workspace_bytes(int64_t n, int64_t p);
+int bi_schur2x2(int pivot, int64_t n, int64_t p,
+                const double* m, int64_t ldm, double* out, int64_t ldo,
+                void* workspace, int64_t workspace_bytes,
+                int* fail_block, void* stream);
+
+/* ------------------------------------------------------------------------
+ * invertor_inplace_by_a (recursive.py:273-333): x <- x^-1 in place by the
+ * pivot-A recursion (Eq. 2) with K3 leaves of order <= leaf_order.
+ * On failure *fail_path receives the recursion path as a string of 'A'/'S'
+ * (A / SchurA) of at most 63 characters.
+ * ---------------------------------------------------------------------- */
+int64_t bi_inplace_by_a_workspace_bytes(int64_t n, int64_t leaf_order);
+int bi_inplace_by_a(int64_t n, double* x, int64_t ldx, int64_t leaf_order,
+                    void* workspace, int64_t workspace_bytes,
+                    char* fail_path, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K4: residual norms for verification (core.residual_norm, core.py:405-414,
+ * in the Frobenius form of the north star).  Writes, for `batch` pairs,
+ * out[2*i] = ||A_i X_i - I||_F^2 and out[2*i+1] = max |A_i X_i - I| (device
+ * pointer, 2*batch doubles).  workspace: bi_residual_workspace_bytes.
+ * ---------------------------------------------------------------------- */
+int64_t bi_residual_workspace_bytes(int64_t n, int batch);
+int bi_residual(int64_t n, int batch,
+                const double* a, int64_t lda, int64_t stride_a,
+                const double* x, int64_t ldx, int64_t stride_x,
+                double* out, void* workspace, int64_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLOCKINV_B200_H */

@@ -1,0 +1,168 @@
+"""ctypes binding of libblockinv_b200.so (the C ABI in include/blockinv_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is visible, every compute entry point raises ``NativeUnavailable``.
+PyTorch is used only for device memory and the current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+from .errors import BlockInvError, DimensionMismatch
+
+LIB_PATH = Path(__file__).resolve().parent / "libblockinv_b200.so"
+
+# (name, restype, argtypes) for every symbol the header declares.
+_c_i64 = ctypes.c_int64
+_c_int = ctypes.c_int
+_vp = ctypes.c_void_p
+_pint = ctypes.POINTER(ctypes.c_int)
+_pdbl = ctypes.POINTER(ctypes.c_double)
+
+SIGNATURES = [
+    ("bi_version", _c_int, []),
+    ("bi_last_error", ctypes.c_char_p, []),
+    ("bi_gemm", _c_int, [_c_i64, _c_i64, _c_i64, _c_int,
+                         _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64,
+                         _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _c_int, _vp]),
+    ("bi_inv_workspace_bytes", _c_i64, [_c_int, _c_i64]),
+    ("bi_inv_batched", _c_int, [_c_int, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64,
+                                _vp, _vp, _c_i64, _vp]),
+    ("bi_engine_create", _c_int, [ctypes.POINTER(_vp), _c_int, ctypes.POINTER(_c_i64), _c_int]),
+    ("bi_engine_workspace_bytes", _c_i64, [_vp]),
+    ("bi_engine_bind", _c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp]),
+    ("bi_engine_run", _c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
+    ("bi_engine_status", _c_int, [_vp, _pint, _pint, _pint]),
+    ("bi_engine_counters", _c_int, [_vp, _c_int, _c_int, _pdbl]),
+    ("bi_engine_tset_square", _c_int, [_vp, _c_int, _c_int, _c_int, ctypes.POINTER(_vp),
+                                       ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)]),
+    ("bi_engine_destroy", _c_int, [_vp]),
+    ("bi_schur2x2_workspace_bytes", _c_i64, [_c_i64, _c_i64]),
+    ("bi_schur2x2", _c_int, [_c_int, _c_i64, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _pint, _vp]),
+    ("bi_inplace_by_a_workspace_bytes", _c_i64, [_c_i64, _c_i64]),
+    ("bi_inplace_by_a", _c_int, [_c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, ctypes.c_char_p, _vp]),
+    ("bi_residual_workspace_bytes", _c_i64, [_c_i64, _c_int]),
+    ("bi_residual", _c_int, [_c_i64, _c_int, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64,
+                             _vp, _vp, _c_i64, _vp]),
+]
+
+BI_OK, BI_ESINGULAR, BI_EDIM, BI_ECUDA, BI_ENCCL, BI_EUNSUPPORTED = range(6)
+
+
+class NativeUnavailable(BlockInvError, RuntimeError):
+    """The CUDA library or a CUDA device is missing (no CPU fallback exists)."""
+
+
+class NativeError(BlockInvError, RuntimeError):
+    """A CUDA/runtime failure reported by the native library."""
+
+
+_lib = None
+
+
+def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load (once) and type the shared library; raises NativeUnavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise NativeUnavailable(
+            f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    lib = ctypes.CDLL(str(p))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    return load_library()
+
+
+def check(rc: int, what: str = "") -> int:
+    """Map a C-ABI status onto the exception taxonomy (errors.py)."""
+    if rc == BI_OK or rc == BI_ESINGULAR:
+        return rc
+    msg = (lib().bi_last_error() or b"").decode(errors="replace")
+    if rc == BI_EDIM:
+        raise DimensionMismatch(f"{what}: {msg}")
+    if rc == BI_EUNSUPPORTED:
+        raise NotImplementedError(f"{what}: {msg}")
+    raise NativeError(f"{what}: status {rc}: {msg}")
+
+
+# ---------------------------------------------------------------------------
+# device plumbing (torch for memory and streams only)
+# ---------------------------------------------------------------------------
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    return _torch
+
+
+def require_device():
+    """Return the current CUDA device; raise NativeUnavailable without one."""
+    load_library()
+    t = torch()
+    if not t.cuda.is_available():
+        raise NativeUnavailable("no CUDA device visible: the B200 library has no CPU fallback")
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return int(torch().cuda.current_stream().cuda_stream)
+
+
+def padded_ld(cols: int) -> int:
+    """Row pitch in elements: multiple of 4 doubles (32 B) for aligned vector loads."""
+    return max(4, (int(cols) + 3) // 4 * 4)
+
+
+def empty_matrix(rows: int, cols: int, batch: int | None = None):
+    """Device float64 matrix (or batch) with padded row pitch; returns the
+    [rows, cols] (or [batch, rows, cols]) view of the padded storage."""
+    t = torch()
+    dev = require_device()
+    ld = padded_ld(cols)
+    if batch is None:
+        return t.empty((rows, ld), dtype=t.float64, device=dev)[:, :cols]
+    return t.empty((batch, rows, ld), dtype=t.float64, device=dev)[:, :, :cols]
+
+
+def to_device(a: np.ndarray):
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 2:
+        d = empty_matrix(a.shape[0], a.shape[1])
+    else:
+        d = empty_matrix(a.shape[1], a.shape[2], batch=a.shape[0])
+    d.copy_(torch().from_numpy(np.ascontiguousarray(a)))
+    return d
+
+
+def workspace(nbytes: int):
+    t = torch()
+    return t.empty((max(int(nbytes), 256),), dtype=t.uint8, device=require_device())
+
+
+def ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+def ld(t) -> int:
+    return int(t.stride(-2))

@@ -1,0 +1,265 @@
+"""Dense FP64 primitives on the B200, behind the reference's signatures
+(/root/reference/pkg/src/blockinv/core.py).
+
+NumPy in / NumPy out, as in the reference; every product runs in the K1
+DMMA GEMM and every inverse in the K3 pivoted Gauss-Jordan kernel of
+libblockinv_b200.so.  There is no CPU compute path.
+"""
+
+from __future__ import annotations
+
+from contextlib import contextmanager
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionMismatch, ScratchTooSmall, SingularBlock, SingularMatrix
+
+# Alias checks on every call (core.py:31-47); benchmarks switch them off.
+debug_checks = True
+
+
+@contextmanager
+def release_mode():
+    """Temporarily disable debug alias checks (core.py:38-47)."""
+    global debug_checks
+    saved = debug_checks
+    debug_checks = False
+    try:
+        yield
+    finally:
+        debug_checks = saved
+
+
+@dataclass
+class OpCounters:
+    """Block-operation tallies (core.py:61-96)."""
+
+    multiplies: int = 0
+    inversions: int = 0
+    reductions: int = 0
+    peak_scratch: int = 0
+    schur_scratch: int = 0
+    nodes: int = 0
+    _current_scratch: int = field(default=0, repr=False)
+
+    def alloc(self, scalars: int) -> None:
+        self._current_scratch += scalars
+        if self._current_scratch > self.peak_scratch:
+            self.peak_scratch = self._current_scratch
+
+    def release(self, scalars: int) -> None:
+        self._current_scratch -= scalars
+
+    def merge(self, other: "OpCounters") -> None:
+        self.multiplies += other.multiplies
+        self.inversions += other.inversions
+        self.reductions += other.reductions
+        self.schur_scratch += other.schur_scratch
+        self.nodes += other.nodes
+        self.peak_scratch = max(self.peak_scratch, other.peak_scratch)
+
+
+def as_matrix(data) -> np.ndarray:
+    """core.py:99-104."""
+    m = np.asarray(data, dtype=np.float64)
+    if m.ndim != 2:
+        raise DimensionMismatch(f"expected a 2-D array, got ndim={m.ndim}")
+    return m
+
+
+def _disjoint(x, y) -> bool:
+    return not np.may_share_memory(x, y) or not np.shares_memory(x, y)
+
+
+# ---------------------------------------------------------------------------
+# device-level building blocks (torch tensors in, torch tensors out)
+# ---------------------------------------------------------------------------
+
+
+def device_gemm(a, b, d, c=None, negate=False):
+    """K1 on device tensors: d = [c] + (+-1) a @ b.  2-D views with unit
+    column stride; `c` may be `d` (in-place accumulate)."""
+    m, k = a.shape
+    n = b.shape[1]
+    if b.shape[0] != k or tuple(d.shape) != (m, n) or (c is not None and tuple(c.shape) != (m, n)):
+        raise DimensionMismatch(f"gemm {tuple(a.shape)} x {tuple(b.shape)} -> {tuple(d.shape)}")
+    L = _lib.lib()
+    rc = L.bi_gemm(m, n, k, -1 if negate else 1,
+                   _lib.ptr(a), _lib.ld(a), 0, _lib.ptr(b), _lib.ld(b), 0,
+                   _lib.ptr(c) if c is not None else None, _lib.ld(c) if c is not None else 0, 0,
+                   _lib.ptr(d), _lib.ld(d), 0, 1, _lib.stream_ptr())
+    _lib.check(rc, "bi_gemm")
+
+
+def device_inverse(blocks, out):
+    """K3 on a device batch: out[i] = inverse(blocks[i]).  `blocks`/`out` are
+    [count, n, n] (or [n, n]) views with unit column stride.  Returns the
+    per-block info array (numpy): 0 ok, c+1 first singular pivot column."""
+    t = _lib.torch()
+    single = blocks.dim() == 2
+    if single:
+        blocks, out = blocks.unsqueeze(0), out.unsqueeze(0)
+    count, n, n2 = blocks.shape
+    if n != n2 or tuple(out.shape) != (count, n, n):
+        raise DimensionMismatch(f"inverse of {tuple(blocks.shape)} into {tuple(out.shape)}")
+    L = _lib.lib()
+    ws = _lib.workspace(L.bi_inv_workspace_bytes(count, n))
+    info = t.zeros((count,), dtype=t.int32, device=blocks.device)
+    rc = L.bi_inv_batched(count, n, _lib.ptr(blocks), _lib.ld(blocks), int(blocks.stride(0)),
+                          _lib.ptr(out), _lib.ld(out), int(out.stride(0)), _lib.ptr(info),
+                          _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "bi_inv_batched")
+    return info.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# reference-signature entry points (NumPy in / NumPy out)
+# ---------------------------------------------------------------------------
+
+
+def multiply(a, b, out, accumulate=False, negate=False, counters: OpCounters | None = None) -> None:
+    """out = (+-1) a @ b, or out += ... when ``accumulate`` (core.py:142-170)."""
+    if a.shape[1] != b.shape[0] or out.shape[0] != a.shape[0] or out.shape[1] != b.shape[1]:
+        raise DimensionMismatch(f"multiply {a.shape} x {b.shape} -> {out.shape}")
+    if debug_checks:
+        assert _disjoint(out, a), "out aliases a"
+        assert _disjoint(out, b), "out aliases b"
+    if out.size:
+        da, db = _lib.to_device(a), _lib.to_device(b)
+        dout = _lib.to_device(out) if accumulate else _lib.empty_matrix(*out.shape)
+        if a.shape[1] == 0:
+            if not accumulate:
+                out[...] = 0.0
+        else:
+            device_gemm(da, db, dout, c=dout if accumulate else None, negate=negate)
+            out[...] = dout.cpu().numpy()
+    if counters is not None:
+        counters.multiplies += 1
+        if accumulate:
+            counters.reductions += 1
+
+
+def schur_accumulate(dest, x, y, counters: OpCounters | None = None) -> None:
+    """dest += x @ y counted as a reduction only (core.py:173-192)."""
+    if x.shape[1] != y.shape[0] or dest.shape != (x.shape[0], y.shape[1]):
+        raise DimensionMismatch(f"schur_accumulate {x.shape} x {y.shape} -> {dest.shape}")
+    if debug_checks:
+        assert _disjoint(dest, x), "dest aliases x"
+        assert _disjoint(dest, y), "dest aliases y"
+    multiply(x, y, dest, accumulate=True)
+    if counters is not None:
+        counters.reductions += 1
+
+
+def multiply_inplace_left(a_inv, target, row_scratch, negate=False, counters=None) -> None:
+    """target <- (+-1) a_inv @ target (core.py:195-225).  The scratch contract
+    is validated as in the reference; the device product needs none."""
+    n = target.shape[0]
+    if a_inv.shape != (n, n):
+        raise DimensionMismatch(f"inplace left {a_inv.shape} on {target.shape}")
+    if row_scratch.shape[0] < n:
+        raise ScratchTooSmall(f"need {n} scalars, have {row_scratch.shape[0]}")
+    res = np.empty_like(target)
+    multiply(np.asarray(a_inv), np.asarray(target), res, negate=negate)
+    target[...] = res
+    if counters is not None:
+        counters.multiplies += 1
+
+
+def multiply_inplace_right(target, a_inv, row_scratch, negate=False, counters=None) -> None:
+    """target <- (+-1) target @ a_inv (core.py:228-253)."""
+    n = target.shape[1]
+    if a_inv.shape != (n, n):
+        raise DimensionMismatch(f"inplace right {target.shape} on {a_inv.shape}")
+    if row_scratch.shape[0] < n:
+        raise ScratchTooSmall(f"need {n} scalars, have {row_scratch.shape[0]}")
+    res = np.empty_like(target)
+    multiply(np.asarray(target), np.asarray(a_inv), res, negate=negate)
+    target[...] = res
+    if counters is not None:
+        counters.multiplies += 1
+
+
+def _invert_host_block(m: np.ndarray) -> tuple[np.ndarray, int]:
+    dm = _lib.to_device(m)
+    dout = _lib.empty_matrix(*m.shape)
+    info = device_inverse(dm, dout)
+    return dout.cpu().numpy(), int(info[0])
+
+
+def invert_small(m, out, counters: OpCounters | None = None) -> None:
+    """Inverse of an order 1-4 block into ``out`` (core.py:350-376) by the K3
+    pivoted GJ kernel; singular -> SingularBlock("A")."""
+    n = m.shape[0]
+    if m.shape != (n, n) or out.shape != (n, n) or not 1 <= n <= 4:
+        raise DimensionMismatch(f"invert_small on {m.shape} -> {out.shape}")
+    inv, info = _invert_host_block(as_matrix(m))
+    if info:
+        raise SingularBlock("A", path=[])
+    out[...] = inv
+    if counters is not None:
+        counters.inversions += 1
+
+
+def gauss_jordan_oracle(m, counters: OpCounters | None = None) -> np.ndarray:
+    """Partial-pivot Gauss-Jordan inverse (core.py:379-402) on the device (K3),
+    same pivot rule and tolerance 1e-12 * n * max|m|; raises SingularMatrix."""
+    m = as_matrix(m)
+    n = m.shape[0]
+    if m.shape[0] != m.shape[1]:
+        raise DimensionMismatch(f"oracle needs a square matrix, got {m.shape}")
+    if n == 0:
+        return np.zeros((0, 0))
+    inv, info = _invert_host_block(m)
+    if info:
+        raise SingularMatrix(f"no pivot in column {info - 1}")
+    if counters is not None:
+        counters.inversions += 1
+    return np.ascontiguousarray(inv)
+
+
+def gpu_invert_sub(block, out) -> None:
+    """The device leaf inverter in the reference's ``invert_sub(block, out)``
+    plugin protocol (schur.py:16-18, 104-111): works on any order, raises
+    SingularBlock.  Passing it to the reference's own ``invert_via_d``
+    drops the B200 leaf kernel into the reference formula."""
+    inv, info = _invert_host_block(as_matrix(block))
+    if info:
+        raise SingularBlock("A", path=[])
+    out[...] = inv
+
+
+def _residual_device(da, dx, batch=False):
+    L = _lib.lib()
+    t = _lib.torch()
+    if not batch:
+        da, dx = da.unsqueeze(0), dx.unsqueeze(0)
+    z, n, _ = da.shape
+    ws = _lib.workspace(L.bi_residual_workspace_bytes(n, z))
+    out = t.zeros((2 * z,), dtype=t.float64, device=da.device)
+    rc = L.bi_residual(n, z, _lib.ptr(da), _lib.ld(da), int(da.stride(0)),
+                       _lib.ptr(dx), _lib.ld(dx), int(dx.stride(0)), _lib.ptr(out),
+                       _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "bi_residual")
+    o = out.cpu().numpy().reshape(z, 2)
+    return np.sqrt(o[:, 0]), o[:, 1]
+
+
+def residual_norm(x, x_inv) -> float:
+    """max |x @ x_inv - I| (core.py:405-414), computed by K1 + K4 on device."""
+    x, x_inv = as_matrix(x), as_matrix(x_inv)
+    if x.shape != x_inv.shape or x.shape[0] != x.shape[1]:
+        raise DimensionMismatch(f"residual_norm {x.shape} vs {x_inv.shape}")
+    _, mx = _residual_device(_lib.to_device(x), _lib.to_device(x_inv))
+    return float(mx[0])
+
+
+def residual_frobenius(x, x_inv) -> float:
+    """||x @ x_inv - I||_F (the north-star residual), on device."""
+    x, x_inv = as_matrix(x), as_matrix(x_inv)
+    if x.shape != x_inv.shape or x.shape[0] != x.shape[1]:
+        raise DimensionMismatch(f"residual_frobenius {x.shape} vs {x_inv.shape}")
+    fro, _ = _residual_device(_lib.to_device(x), _lib.to_device(x_inv))
+    return float(fro[0])

@@ -1,0 +1,130 @@
+// Shared definitions for the B200 blockwise-inversion library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libblockinv_b200 is built for sm_100a only"
+#endif
+
+namespace bi {
+
+// ---------------------------------------------------------------------------
+// error plumbing (C-ABI status codes, see include/blockinv_b200.h)
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+const char* get_error();
+
+struct Status {
+  int code = 0;
+  static Status ok() { return Status{}; }
+};
+
+#define BI_CUDA_TRY(expr)                                                          \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      ::bi::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+      return 3;                                                                    \
+    }                                                                              \
+  } while (0)
+
+#define BI_REQUIRE(cond, msg)                                                      \
+  do {                                                                             \
+    if (!(cond)) {                                                                 \
+      ::bi::set_error(msg);                                                        \
+      return 2;                                                                    \
+    }                                                                              \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// K1 descriptors: D = beta*C + sign*A*B, strided batched, optional output
+// column remap (the Gauss-Jordan trailing update skips the panel columns).
+// ---------------------------------------------------------------------------
+struct GemmDesc {
+  const double* A;
+  const double* B;
+  const double* C;  // may be null (beta = 0) or equal to D
+  double* D;
+  int64_t lda, ldb, ldc, ldd;
+  int64_t sA, sB, sC, sD;  // batch strides in elements
+  int M, N, K, batch;
+  int neg;       // 1: alpha = -1
+  int skip_at;   // output column n >= skip_at is stored at n + skip_len
+  int skip_len;
+  int tiles_m, tiles_n;  // filled by finalize_descs
+  int tile_begin;        // prefix over descriptors (filled by finalize_descs)
+};
+
+constexpr int kGemmInline = 4;  // descriptors passed by value in kernel params
+
+struct GemmLaunch {
+  const GemmDesc* descs;  // device array when count > kGemmInline
+  int count;
+  int total_tiles;
+  GemmDesc inl[kGemmInline];
+};
+
+// Tile sizes of the DMMA kernel.
+constexpr int kBM = 128, kBN = 128, kBK = 16;
+
+// Fills tiles_m/tiles_n/tile_begin; returns total tiles.
+int finalize_descs(GemmDesc* d, int count);
+// Launch on `stream`. `d_descs` may be null when count <= kGemmInline.
+cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int count,
+                        cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// K3 batched pivoted Gauss-Jordan, one group of equal-order blocks.
+// Blocks are addressed either by pointer arrays (device) or base + stride.
+// ---------------------------------------------------------------------------
+struct InvGroup {
+  int n;      // block order
+  int count;  // number of blocks
+  const double* src_base;
+  int64_t src_stride, ld_src;
+  const double* const* src_ptrs;  // optional device array [count]
+  const int64_t* src_lds;         // optional device array [count]
+  double* dst_base;
+  int64_t dst_stride, ld_dst;
+  double* const* dst_ptrs;  // optional
+  const int64_t* dst_lds;   // optional
+  // scratch (device), laid out by inv_group_layout
+  double* W;        // count * n * ldw
+  int64_t ldw;
+  double* tmp;      // count * 32 * ldw
+  int* perm;        // count * n
+  int* flags;       // count * n
+  unsigned long long* maxabs;  // count (bit pattern of max|.|)
+  int* info;        // count (device; caller-visible)
+};
+
+int64_t inv_group_scratch_bytes(int n, int count);
+// Assign scratch pointers from `base` (needs inv_group_scratch_bytes bytes).
+void inv_group_layout(InvGroup& g, void* base);
+// Number of panels and the per-panel trailing-update descriptors (host);
+// descriptors are strided over the group's workspace slab.
+int inv_group_panels(const InvGroup& g);
+void inv_group_panel_desc(const InvGroup& g, int panel, GemmDesc* out);
+// Full inversion of the group on `stream`: init, load, panels (+updates), store.
+// `d_panel_descs`: optional device copy of the panel descriptors (count = panels);
+// when null, descriptors go inline in the kernel parameters.
+cudaError_t launch_inv_group(const InvGroup& g, const GemmDesc* d_panel_descs,
+                             cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// K4 residual
+// ---------------------------------------------------------------------------
+cudaError_t launch_residual(int64_t n, int batch, const double* a, int64_t lda, int64_t sa,
+                            const double* x, int64_t ldx, int64_t sx, double* out,
+                            double* scratch, cudaStream_t stream);
+
+// Set kernel attributes (dynamic smem, cluster sizes) once per process.
+cudaError_t init_attributes();
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+}  // namespace bi

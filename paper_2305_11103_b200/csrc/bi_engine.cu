@@ -1,0 +1,626 @@
+// Native step scheduler for the 2^k-diagonal-block engine (run_inversion).
+//
+// Reference: /root/reference/pkg/src/blockinv/engine.py:73-162 (stepid ->
+// loopid -> action), :289-446 (the three actions), storage.py:166-262,
+// 391-411 (M_inv and the provisional sets T_l).
+//
+// B200 design:
+//  * device-resident, coordinate-aligned layout: M and M_inv are padded
+//    row-major n x n buffers; T_l is stored as the batch of level-l quad
+//    squares (side = quad span, contiguous, ld padded to 4) with S_D at A's
+//    position, R at B's, L at C's and S_A at D's -- every operand of every
+//    step is a window at the same block coordinates as in M;
+//  * each step is a fixed list of device ops built once at bind time:
+//      diag      -> K3 batched pivoted GJ over all N_b x batch leaves
+//      arrows    -> K1 launch {R=-A^-1 B, L=-D^-1 C}, K1 launch {S_D=A+B L, S_A=D+C R}
+//      assemble  -> diag on T_cid S, then per pass one K1 launch {down, up}
+//    GEMM descriptors of equal shape and constant pointer stride are merged
+//    into strided batches; everything is uploaded once and the whole step
+//    range is replayed as one CUDA graph;
+//  * singular leaves are recorded per diag step on the device and resolved
+//    to (step, quad, matrix) after the range (no host syncs inside it).
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/blockinv_b200.h"
+#include "bi_common.cuh"
+
+namespace bi {
+
+struct StepAct {
+  int kind;  // 0 diag, 1 arrows, 2 assemble
+  int from_tset;
+  int cid, sid, depth;
+};
+
+static int loopid_decode(int stepid, int nblocks, StepAct* out) {
+  // engine.py:77-90 (loopid) and :117-157 (decode rules)
+  int width = 0;
+  while ((1 << width) < nblocks) ++width;
+  width += 1;
+  std::vector<int> nz;
+  for (int b = width - 1; b >= 0; --b)
+    if ((stepid >> b) & 1) nz.push_back(b + 1);
+  if (nz.empty()) return 2;
+  const int last = nz.back();
+  StepAct a{};
+  if (nz.size() == 1) {
+    a.kind = last == 1 ? 0 : 1;
+    a.from_tset = 0;
+    a.sid = last - 1;
+  } else {
+    a.cid = nz[nz.size() - 2] - 1;
+    a.from_tset = 1;
+    if (last == 1) {
+      int run = 1;
+      while (run < (int)nz.size() && nz[nz.size() - run - 1] == run + 1) ++run;
+      a.kind = 2;
+      a.depth = run - 1;
+    } else {
+      a.kind = 1;
+      a.sid = last - 1;
+    }
+  }
+  *out = a;
+  return 0;
+}
+
+// Merge consecutive descriptors that differ only by a constant pointer stride.
+static std::vector<GemmDesc> merge_descs(const std::vector<GemmDesc>& in) {
+  std::vector<GemmDesc> out;
+  for (const GemmDesc& d : in) {
+    if (!out.empty()) {
+      GemmDesc& p = out.back();
+      const bool same = p.M == d.M && p.N == d.N && p.K == d.K && p.lda == d.lda && p.ldb == d.ldb &&
+                        p.ldc == d.ldc && p.ldd == d.ldd && p.neg == d.neg && p.skip_len == d.skip_len &&
+                        p.skip_at == d.skip_at && (p.C == nullptr) == (d.C == nullptr);
+      if (same) {
+        const int64_t dA = d.A - p.A, dB = d.B - p.B, dD = d.D - p.D, dC = d.C ? d.C - p.C : 0;
+        if (p.batch == 1) {
+          p.sA = dA;
+          p.sB = dB;
+          p.sC = dC;
+          p.sD = dD;
+          p.batch = 2;
+          continue;
+        }
+        const int64_t b = p.batch;
+        if (dA == b * p.sA && dB == b * p.sB && dD == b * p.sD && dC == b * p.sC) {
+          p.batch += 1;
+          continue;
+        }
+      }
+    }
+    GemmDesc c = d;
+    c.batch = 1;
+    c.sA = c.sB = c.sC = c.sD = 0;
+    out.push_back(c);
+  }
+  return out;
+}
+
+}  // namespace bi
+
+using namespace bi;
+
+namespace {
+
+struct Op {
+  int kind;      // 0 = inversion group, 1 = gemm launch
+  int index;     // inv group index / gemm launch index
+};
+
+struct GemmLaunchRec {
+  int first, count;  // into the descriptor table
+};
+
+struct InvRec {
+  InvGroup g;           // device pointers filled at bind
+  int panel_first;      // into descriptor table (per-panel update descs)
+  int diag_step_index;  // which diag step (for info reporting)
+  std::vector<int> item_block;   // block index p of each item
+  std::vector<int> item_matrix;  // matrix index z of each item
+  int info_offset;      // into the info region (ints)
+};
+
+struct Window {
+  double* p;
+  int64_t ld;
+};
+
+}  // namespace
+
+struct bi_engine {
+  int nb = 0, Z = 0, k = 0, nsteps = 0;
+  std::vector<int64_t> sizes, off;
+  int64_t n = 0;
+  // bound buffers
+  const double* M = nullptr;
+  int64_t ldm = 0, sm = 0;
+  double* Minv = nullptr;
+  int64_t ldi = 0, si = 0;
+  char* ws = nullptr;
+  int64_t ws_bytes = 0;
+  // layout
+  struct Sq {
+    int64_t off, side, ld;
+  };
+  std::vector<std::vector<Sq>> tsq;  // [level][quad]
+  int64_t t_matrix = 0;              // elements per matrix (all levels)
+  int64_t t_bytes = 0, inv_scratch = 0, info_ints = 0, meta_bytes = 0;
+  double* T = nullptr;
+  void* inv_base = nullptr;
+  int* info = nullptr;
+  GemmDesc* d_descs = nullptr;
+  void* d_ptrs = nullptr;
+  // schedule
+  std::vector<std::vector<Op>> step_ops;  // [stepid]
+  std::vector<GemmDesc> descs;            // host copy of the table
+  std::vector<GemmLaunchRec> launches;
+  std::vector<InvRec> invs;
+  std::vector<int> diag_steps;            // stepids of diag actions
+  bool bound = false;
+  cudaStream_t last_stream = nullptr;
+  cudaStream_t capture_stream = nullptr;
+  std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+  int last_first = 1, last_last = 0;
+
+  void* meta_dev = nullptr;
+  int64_t meta_cap = 0;
+
+  ~bi_engine() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    if (capture_stream) cudaStreamDestroy(capture_stream);
+    if (meta_dev) cudaFree(meta_dev);
+  }
+
+  Window tset_window(int level, int z, int r0, int r1, int c0, int c1) const {
+    const int lo = std::min(r0, c0);
+    const int qp = lo >> level;
+    const Sq& s = tsq[level][qp];
+    const int64_t origin = off[(size_t)qp << level];
+    double* base = T + (int64_t)z * t_matrix + s.off;
+    (void)r1;
+    (void)c1;
+    return Window{base + (off[r0] - origin) * s.ld + (off[c0] - origin), s.ld};
+  }
+  Window m_window(int z, int r0, int c0) const {
+    return Window{const_cast<double*>(M) + (int64_t)z * sm + off[r0] * ldm + off[c0], ldm};
+  }
+  Window minv_window(int z, int r0, int c0) const {
+    return Window{Minv + (int64_t)z * si + off[r0] * ldi + off[c0], ldi};
+  }
+  Window source(const StepAct& a, int z, int r0, int r1, int c0, int c1) const {
+    return a.from_tset ? tset_window(a.cid, z, r0, r1, c0, c1) : m_window(z, r0, c0);
+  }
+};
+
+static int64_t align256(int64_t v) { return round_up(v, 256); }
+
+extern "C" int bi_engine_create(bi_engine** out, int nblocks, const int64_t* sizes, int batch) {
+  BI_REQUIRE(out != nullptr && sizes != nullptr, "null argument");
+  BI_REQUIRE(nblocks >= 1 && (nblocks & (nblocks - 1)) == 0,
+             "number of diagonal blocks must be a power of two");
+  BI_REQUIRE(batch >= 1, "batch must be >= 1");
+  auto e = std::make_unique<bi_engine>();
+  e->nb = nblocks;
+  e->Z = batch;
+  while ((1 << e->k) < nblocks) ++e->k;
+  e->nsteps = 2 * nblocks - 1;
+  e->off.push_back(0);
+  int64_t maxb = 0;
+  for (int i = 0; i < nblocks; ++i) {
+    BI_REQUIRE(sizes[i] >= 1, "block sizes must be >= 1");
+    e->sizes.push_back(sizes[i]);
+    e->off.push_back(e->off.back() + sizes[i]);
+    maxb = std::max(maxb, sizes[i]);
+  }
+  BI_REQUIRE(maxb <= 8192, "diagonal blocks above order 8192 are not supported by the leaf kernel");
+  e->n = e->off.back();
+  // T-set layout (per matrix)
+  e->tsq.resize(e->k + 1);
+  int64_t t = 0;
+  for (int lv = 1; lv <= e->k; ++lv) {
+    const int nq = nblocks >> lv;
+    for (int g = 0; g < nq; ++g) {
+      const int64_t side = e->off[(size_t)(g + 1) << lv] - e->off[(size_t)g << lv];
+      const int64_t ld = round_up(side, 4);
+      e->tsq[lv].push_back({t, side, ld});
+      t += round_up(side * ld, 32);
+    }
+  }
+  e->t_matrix = t;
+  e->t_bytes = align256(t * 8 * (int64_t)batch);
+  // leaf scratch: the largest equal-size group of one diag step
+  std::map<int64_t, int> cnt;
+  for (int64_t s : e->sizes) cnt[s] += batch;
+  int64_t scratch = 0;
+  for (auto& kv : cnt) scratch = std::max(scratch, inv_group_scratch_bytes((int)kv.first, kv.second));
+  e->inv_scratch = align256(scratch);
+  e->info_ints = (int64_t)nblocks * nblocks * batch;  // nblocks diag steps x leaves
+  // metadata upper bound (descriptors + pointer tables); computed exactly at bind
+  *out = e.release();
+  return 0;
+}
+
+extern "C" int64_t bi_engine_workspace_bytes(const bi_engine* e) {
+  if (!e) return -1;
+  // schedule metadata (descriptor and pointer tables) is engine-owned device memory
+  return e->t_bytes + e->inv_scratch + align256(e->info_ints * 4);
+}
+
+static int build_schedule(bi_engine* e) {
+  e->step_ops.assign(e->nsteps + 1, {});
+  e->descs.clear();
+  e->launches.clear();
+  e->invs.clear();
+  e->diag_steps.clear();
+  const int nb = e->nb, Z = e->Z;
+  const auto& off = e->off;
+  auto add_launch = [&](const std::vector<GemmDesc>& raw) -> int {
+    std::vector<GemmDesc> m = merge_descs(raw);
+    GemmLaunchRec rec{(int)e->descs.size(), (int)m.size()};
+    finalize_descs(m.data(), (int)m.size());
+    e->descs.insert(e->descs.end(), m.begin(), m.end());
+    e->launches.push_back(rec);
+    return (int)e->launches.size() - 1;
+  };
+  auto gemm = [](Window a, Window b, const double* c, int64_t ldc, Window d, int64_t M, int64_t N,
+                 int64_t K, int neg) {
+    GemmDesc g{};
+    g.A = a.p;
+    g.lda = a.ld;
+    g.B = b.p;
+    g.ldb = b.ld;
+    g.C = c;
+    g.ldc = c ? ldc : 0;
+    g.D = d.p;
+    g.ldd = d.ld;
+    g.M = (int)M;
+    g.N = (int)N;
+    g.K = (int)K;
+    g.batch = 1;
+    g.neg = neg;
+    g.skip_at = INT32_MAX;
+    g.skip_len = 0;
+    return g;
+  };
+  int diag_index = 0;
+  int info_cursor = 0;
+  for (int stepid = 1; stepid <= e->nsteps; ++stepid) {
+    StepAct a;
+    loopid_decode(stepid, nb, &a);
+    auto& ops = e->step_ops[stepid];
+    if (a.kind == 0 || a.kind == 2) {
+      // diag: group leaves (z, p) by block size
+      std::map<int64_t, std::vector<std::pair<int, int>>> groups;
+      for (int z = 0; z < Z; ++z)
+        for (int p = 0; p < nb; ++p) groups[e->sizes[p]].push_back({z, p});
+      for (auto& kv : groups) {
+        InvRec r{};
+        r.g.n = (int)kv.first;
+        r.g.count = (int)kv.second.size();
+        r.diag_step_index = diag_index;
+        r.info_offset = info_cursor;
+        info_cursor += r.g.count;
+        for (auto& zp : kv.second) {
+          r.item_matrix.push_back(zp.first);
+          r.item_block.push_back(zp.second);
+        }
+        r.panel_first = -1;
+        e->invs.push_back(std::move(r));
+        ops.push_back({0, (int)e->invs.size() - 1});
+      }
+      e->diag_steps.push_back(stepid);
+      ++diag_index;
+      if (a.kind == 2) {
+        for (int lv = 1; lv <= a.depth; ++lv) {
+          std::vector<GemmDesc> raw;
+          for (int z = 0; z < Z; ++z)
+            for (int g = 0; g < (nb >> lv); ++g) {
+              const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+              const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
+              // down: Minv[D, A] = L * Minv[A, A]
+              raw.push_back(gemm(e->tset_window(lv, z, mid, last, first, mid), e->minv_window(z, first, first),
+                                 nullptr, 0, e->minv_window(z, mid, first), hd, ha, ha, 0));
+            }
+          for (int z = 0; z < Z; ++z)
+            for (int g = 0; g < (nb >> lv); ++g) {
+              const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+              const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
+              // up: Minv[A, D] = R * Minv[D, D]
+              raw.push_back(gemm(e->tset_window(lv, z, first, mid, mid, last), e->minv_window(z, mid, mid),
+                                 nullptr, 0, e->minv_window(z, first, mid), ha, hd, hd, 0));
+            }
+          ops.push_back({1, add_launch(raw)});
+        }
+      }
+    } else {
+      const int lv = a.sid;
+      std::vector<GemmDesc> l1, l2;
+      for (int kind = 0; kind < 2; ++kind)
+        for (int z = 0; z < Z; ++z)
+          for (int g = 0; g < (nb >> lv); ++g) {
+            const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+            const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
+            Window B = e->source(a, z, first, mid, mid, last);
+            Window C = e->source(a, z, mid, last, first, mid);
+            Window R = e->tset_window(lv, z, first, mid, mid, last);
+            Window L = e->tset_window(lv, z, mid, last, first, mid);
+            if (kind == 0) {  // R = -A^-1 B
+              l1.push_back(gemm(e->minv_window(z, first, first), B, nullptr, 0, R, ha, hd, ha, 1));
+            } else {  // L = -D^-1 C
+              l1.push_back(gemm(e->minv_window(z, mid, mid), C, nullptr, 0, L, hd, ha, hd, 1));
+            }
+          }
+      for (int kind = 0; kind < 2; ++kind)
+        for (int z = 0; z < Z; ++z)
+          for (int g = 0; g < (nb >> lv); ++g) {
+            const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+            const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
+            Window Aw = e->source(a, z, first, mid, first, mid);
+            Window B = e->source(a, z, first, mid, mid, last);
+            Window C = e->source(a, z, mid, last, first, mid);
+            Window Dw = e->source(a, z, mid, last, mid, last);
+            Window R = e->tset_window(lv, z, first, mid, mid, last);
+            Window L = e->tset_window(lv, z, mid, last, first, mid);
+            Window SD = e->tset_window(lv, z, first, mid, first, mid);
+            Window SA = e->tset_window(lv, z, mid, last, mid, last);
+            if (kind == 0) {  // S_D = A + B L
+              l2.push_back(gemm(B, L, Aw.p, Aw.ld, SD, ha, ha, hd, 0));
+            } else {  // S_A = D + C R
+              l2.push_back(gemm(C, R, Dw.p, Dw.ld, SA, hd, hd, ha, 0));
+            }
+          }
+      ops.push_back({1, add_launch(l1)});
+      ops.push_back({1, add_launch(l2)});
+    }
+  }
+  return 0;
+}
+
+extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_t stride_m, double* minv,
+                              int64_t ldi, int64_t stride_i, void* workspace, int64_t workspace_bytes,
+                              void* stream) {
+  BI_REQUIRE(e != nullptr, "null engine");
+  BI_REQUIRE(m && minv && workspace, "null buffer");
+  BI_REQUIRE(ldm >= e->n && ldi >= e->n, "leading dimension smaller than the matrix order");
+  BI_REQUIRE(workspace_bytes >= bi_engine_workspace_bytes(e), "workspace too small");
+  for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+  e->graphs.clear();
+  e->M = m;
+  e->ldm = ldm;
+  e->sm = stride_m;
+  e->Minv = minv;
+  e->ldi = ldi;
+  e->si = stride_i;
+  e->ws = static_cast<char*>(workspace);
+  e->ws_bytes = workspace_bytes;
+  char* p = e->ws;
+  e->T = reinterpret_cast<double*>(p);
+  p += e->t_bytes;
+  e->inv_base = p;
+  p += e->inv_scratch;
+  e->info = reinterpret_cast<int*>(p);
+  p += align256(e->info_ints * 4);
+  BI_CUDA_TRY(init_attributes());
+
+  int rc = build_schedule(e);
+  if (rc) return rc;
+  // inversion groups: scratch, info, pointer tables, panel descriptors
+  std::vector<char> host_meta;
+  auto reserve = [&](int64_t bytes) {
+    int64_t o = align256((int64_t)host_meta.size());
+    host_meta.resize(o + bytes);
+    return o;
+  };
+  // panel descriptors appended to e->descs
+  struct PtrTab {
+    int64_t src, srcld, dst, dstld;
+  };
+  std::vector<PtrTab> tabs;
+  for (InvRec& r : e->invs) {
+    inv_group_layout(r.g, e->inv_base);
+    r.g.info = e->info + r.info_offset;
+    const int panels = inv_group_panels(r.g);
+    r.panel_first = (int)e->descs.size();
+    for (int pnl = 0; pnl < panels; ++pnl) {
+      GemmDesc d;
+      inv_group_panel_desc(r.g, pnl, &d);
+      e->descs.push_back(d);
+    }
+    tabs.push_back({reserve(r.g.count * 8), reserve(r.g.count * 8), reserve(r.g.count * 8),
+                    reserve(r.g.count * 8)});
+  }
+  const int64_t desc_off = reserve((int64_t)e->descs.size() * sizeof(GemmDesc));
+  if ((int64_t)host_meta.size() > e->meta_cap) {
+    if (e->meta_dev) cudaFree(e->meta_dev);
+    e->meta_dev = nullptr;
+    e->meta_cap = 0;
+    BI_CUDA_TRY(cudaMalloc(&e->meta_dev, host_meta.size()));
+    e->meta_cap = (int64_t)host_meta.size();
+  }
+  char* meta = static_cast<char*>(e->meta_dev);
+  // fill tables (device addresses relative to meta)
+  int diag_i = 0;
+  for (size_t i = 0; i < e->invs.size(); ++i) {
+    InvRec& r = e->invs[i];
+    const int stepid = e->diag_steps[r.diag_step_index];
+    StepAct a;
+    loopid_decode(stepid, e->nb, &a);
+    auto* src = reinterpret_cast<const double**>(host_meta.data() + tabs[i].src);
+    auto* srcld = reinterpret_cast<int64_t*>(host_meta.data() + tabs[i].srcld);
+    auto* dst = reinterpret_cast<double**>(host_meta.data() + tabs[i].dst);
+    auto* dstld = reinterpret_cast<int64_t*>(host_meta.data() + tabs[i].dstld);
+    for (int it = 0; it < r.g.count; ++it) {
+      const int z = r.item_matrix[it], pb = r.item_block[it];
+      Window s = e->source(a, z, pb, pb + 1, pb, pb + 1);
+      Window d = e->minv_window(z, pb, pb);
+      src[it] = s.p;
+      srcld[it] = s.ld;
+      dst[it] = d.p;
+      dstld[it] = d.ld;
+    }
+    r.g.src_ptrs = reinterpret_cast<const double* const*>(meta + tabs[i].src);
+    r.g.src_lds = reinterpret_cast<const int64_t*>(meta + tabs[i].srcld);
+    r.g.dst_ptrs = reinterpret_cast<double* const*>(meta + tabs[i].dst);
+    r.g.dst_lds = reinterpret_cast<const int64_t*>(meta + tabs[i].dstld);
+    ++diag_i;
+  }
+  std::memcpy(host_meta.data() + desc_off, e->descs.data(), e->descs.size() * sizeof(GemmDesc));
+  e->d_descs = reinterpret_cast<GemmDesc*>(meta + desc_off);
+  BI_CUDA_TRY(cudaMemcpyAsync(meta, host_meta.data(), host_meta.size(), cudaMemcpyHostToDevice,
+                              static_cast<cudaStream_t>(stream)));
+  BI_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  e->bound = true;
+  return 0;
+}
+
+static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s) {
+  for (int stepid = first; stepid <= last; ++stepid) {
+    for (const Op& op : e->step_ops[stepid]) {
+      cudaError_t err;
+      if (op.kind == 0) {
+        const InvRec& r = e->invs[op.index];
+        err = launch_inv_group(r.g, e->d_descs + r.panel_first, s);
+      } else {
+        const GemmLaunchRec& L = e->launches[op.index];
+        err = launch_gemm(e->descs.data() + L.first, e->d_descs + L.first, L.count, s);
+      }
+      if (err != cudaSuccess) return err;
+    }
+  }
+  return cudaSuccess;
+}
+
+extern "C" int bi_engine_run(bi_engine* e, int first_step, int last_step, int use_graph, void* stream) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step,
+             "stepid outside 1..N_s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  e->last_stream = s;
+  e->last_first = first_step;
+  e->last_last = last_step;
+  if (!use_graph) {
+    BI_CUDA_TRY(enqueue_steps(e, first_step, last_step, s));
+    return 0;
+  }
+  auto key = std::make_pair(first_step, last_step);
+  auto it = e->graphs.find(key);
+  if (it == e->graphs.end()) {
+    if (!e->capture_stream) BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->capture_stream, cudaStreamNonBlocking));
+    BI_CUDA_TRY(cudaStreamBeginCapture(e->capture_stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t err = enqueue_steps(e, first_step, last_step, e->capture_stream);
+    cudaGraph_t graph = nullptr;
+    cudaError_t err2 = cudaStreamEndCapture(e->capture_stream, &graph);
+    if (err != cudaSuccess || err2 != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      set_error(std::string("graph capture failed: ") + cudaGetErrorString(err != cudaSuccess ? err : err2));
+      return 3;
+    }
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t err3 = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    BI_CUDA_TRY(err3);
+    it = e->graphs.emplace(key, exec).first;
+  }
+  BI_CUDA_TRY(cudaGraphLaunch(it->second, s));
+  return 0;
+}
+
+extern "C" int bi_engine_status(bi_engine* e, int* fail_step, int* fail_quad, int* fail_matrix) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_CUDA_TRY(cudaStreamSynchronize(e->last_stream));
+  std::vector<int> info(e->info_ints);
+  BI_CUDA_TRY(cudaMemcpy(info.data(), e->info, info.size() * 4, cudaMemcpyDeviceToHost));
+  if (fail_step) *fail_step = 0;
+  if (fail_quad) *fail_quad = -1;
+  if (fail_matrix) *fail_matrix = -1;
+  // earliest executed diag step, then matrix, then block (engine.py:313-330 order)
+  for (size_t di = 0; di < e->diag_steps.size(); ++di) {
+    const int stepid = e->diag_steps[di];
+    if (stepid < e->last_first || stepid > e->last_last) continue;
+    int best_z = -1, best_p = -1;
+    for (const InvRec& r : e->invs) {
+      if (r.diag_step_index != (int)di) continue;
+      for (int it = 0; it < r.g.count; ++it) {
+        if (info[r.info_offset + it] == 0) continue;
+        const int z = r.item_matrix[it], p = r.item_block[it];
+        if (best_z < 0 || z < best_z || (z == best_z && p < best_p)) {
+          best_z = z;
+          best_p = p;
+        }
+      }
+    }
+    if (best_z >= 0) {
+      if (fail_step) *fail_step = stepid;
+      if (fail_quad) *fail_quad = best_p;
+      if (fail_matrix) *fail_matrix = best_z;
+      set_error("singular diagonal block");
+      return 1;
+    }
+  }
+  return 0;
+}
+
+extern "C" int bi_engine_counters(const bi_engine* e, int first_step, int last_step, double out[5]) {
+  BI_REQUIRE(e && out, "null argument");
+  BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps, "stepid outside 1..N_s");
+  double mult = 0, invs = 0, red = 0, gflops = 0, lflops = 0;
+  const auto& off = e->off;
+  for (int stepid = first_step; stepid <= last_step; ++stepid) {
+    StepAct a;
+    loopid_decode(stepid, e->nb, &a);
+    if (a.kind == 0 || a.kind == 2) {
+      invs += e->nb;  // engine.py:317
+      for (int64_t s : e->sizes) lflops += 2.0 * (double)s * s * s;
+    }
+    auto quads = [&](int lv, auto fn) {
+      for (int g = 0; g < (e->nb >> lv); ++g) {
+        const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+        fn((double)(off[mid] - off[first]), (double)(off[last] - off[mid]));
+      }
+    };
+    if (a.kind == 1) {
+      quads(a.sid, [&](double ha, double hd) {
+        mult += 2;  // engine.py:344-345
+        red += 2;
+        gflops += 2.0 * (ha * ha * hd + hd * hd * ha + ha * hd * ha + hd * ha * hd);
+      });
+    } else if (a.kind == 2) {
+      for (int lv = 1; lv <= a.depth; ++lv)
+        quads(lv, [&](double ha, double hd) {
+          mult += 2;  // engine.py:411
+          gflops += 2.0 * (hd * ha * ha + ha * hd * hd);
+        });
+    }
+  }
+  out[0] = mult;
+  out[1] = invs;
+  out[2] = red;
+  out[3] = gflops * e->Z;
+  out[4] = lflops * e->Z;
+  return 0;
+}
+
+extern "C" int bi_engine_tset_square(const bi_engine* e, int level, int quad, int matrix, double** ptr,
+                                     int64_t* ld, int64_t* side) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(level >= 1 && level <= e->k && quad >= 0 && quad < (e->nb >> level) && matrix >= 0 &&
+                 matrix < e->Z,
+             "tset index out of range");
+  const auto& s = e->tsq[level][quad];
+  *ptr = e->T + (int64_t)matrix * e->t_matrix + s.off;
+  *ld = s.ld;
+  *side = s.side;
+  return 0;
+}
+
+extern "C" int bi_engine_destroy(bi_engine* e) {
+  delete e;
+  return 0;
+}

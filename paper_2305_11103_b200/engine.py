@@ -1,0 +1,374 @@
+"""Step-scheduled inversion of a matrix partitioned into 2**k diagonal blocks,
+on the B200.
+
+Mirrors /root/reference/pkg/src/blockinv/engine.py: the same stepid -> loopid
+-> action schedule (engine.py:73-162) and the same public entry points, with
+the step interpreter replaced by the native scheduler in libblockinv_b200.so
+(``bi_engine_*``).  All state -- M, M_inv and every provisional set T_l --
+stays resident in HBM for the whole run; a run is one CUDA-graph replay.
+
+Extension (allowed by SURVEY 8d for config 2): ``run_inversion_batch`` inverts
+a batch of matrices that share one partition in lock-step, so every leaf /
+GEMM launch covers the whole batch.
+"""
+
+from __future__ import annotations
+
+import os
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import OpCounters
+from .errors import (
+    BlockShapeMismatch,
+    DimensionMismatch,
+    MalformedLoopid,
+    OutOfRange,
+    SchemeMismatch,
+    SingularBlock,
+)
+from .partition import PartitionScheme, make_partition, partition_from_sizes
+from .storage import BlockMatrix, MemoryBlockStore
+
+INVERT_DIAGONALS = "invert_diagonals"
+ARROWS_AND_SCHUR = "arrows_and_schur"
+SCHUR_DIAG_AND_ASSEMBLE = "schur_diag_and_assemble"
+
+
+def resolve_workers(explicit: int | None = None) -> int:
+    """Explicit argument beats INVERTOR_WORKERS (engine.py:58-65).  On the
+    B200 build the value is validated and recorded; every step is a single
+    device-wide batched launch, so the result does not depend on it."""
+    if explicit is not None:
+        if explicit < 1:
+            raise ValueError(f"workers must be >= 1, got {explicit}")
+        return explicit
+    env = os.environ.get("INVERTOR_WORKERS", "").strip()
+    return max(int(env), 1) if env else 1
+
+
+# ---------------------------------------------------------------------------
+# schedule (host integer logic; the native scheduler decodes identically)
+# ---------------------------------------------------------------------------
+
+
+def total_steps(blocksize: int) -> int:
+    """engine.py:73-74."""
+    return 2 * blocksize - 1
+
+
+def loopid_for_step(stepid: int, blocksize: int) -> list[int]:
+    """Descending 1-based set-bit positions of stepid, zero-padded to
+    log2(blocksize)+1 entries (engine.py:77-90)."""
+    if blocksize < 1 or blocksize & (blocksize - 1):
+        raise OutOfRange(f"blocksize must be a power of two, got {blocksize}")
+    if not 1 <= stepid <= total_steps(blocksize):
+        raise OutOfRange(f"stepid {stepid} outside 1..{total_steps(blocksize)}")
+    width = blocksize.bit_length()
+    bits = [b + 1 for b in range(width - 1, -1, -1) if (stepid >> b) & 1]
+    return bits + [0] * (width - len(bits))
+
+
+@dataclass(frozen=True)
+class StepAction:
+    """Decoded meaning of one step (engine.py:93-107)."""
+
+    kind: str
+    source: str
+    cid: int | None = None
+    sid: int | None = None
+    depth: int = 0
+
+
+@dataclass(frozen=True)
+class StepPlan:
+    stepid: int
+    loopid: tuple
+    action: StepAction
+
+
+def decode_step(loopid) -> StepAction:
+    """The loopid rules of engine.py:117-157."""
+    loopid = list(loopid)
+    nz: list[int] = []
+    zero_seen = False
+    for v in loopid:
+        if v == 0:
+            zero_seen = True
+        elif zero_seen or v < 0:
+            raise MalformedLoopid(f"{loopid}: zeros only as suffix")
+        else:
+            nz.append(v)
+    if not nz:
+        raise MalformedLoopid(f"{loopid}: no nonzero elements")
+    if any(x <= y for x, y in zip(nz, nz[1:])):
+        raise MalformedLoopid(f"{loopid}: prefix not strictly decreasing")
+    last = nz[-1]
+    if len(nz) == 1:
+        if last == 1:
+            return StepAction(INVERT_DIAGONALS, "matrix")
+        return StepAction(ARROWS_AND_SCHUR, "matrix", sid=last - 1)
+    cid = nz[-2] - 1
+    if last == 1:
+        run = 1
+        while run < len(nz) and nz[-run - 1] == run + 1:
+            run += 1
+        return StepAction(SCHUR_DIAG_AND_ASSEMBLE, "tset", cid=cid, depth=run - 1)
+    return StepAction(ARROWS_AND_SCHUR, "tset", cid=cid, sid=last - 1)
+
+
+def step_plan(stepid: int, blocksize: int) -> StepPlan:
+    loopid = loopid_for_step(stepid, blocksize)
+    return StepPlan(stepid, tuple(loopid), decode_step(loopid))
+
+
+def updown_iteration_map(block_row: int, block_col: int) -> int:
+    """1 + popcount((row-1) xor (col-1)) (engine.py:165-170)."""
+    if block_row < 1 or block_col < 1:
+        raise OutOfRange("block coordinates are 1-based")
+    return 1 + bin((block_row - 1) ^ (block_col - 1)).count("1")
+
+
+# ---------------------------------------------------------------------------
+# blocked products (engine.py:178-249) -- the block structure is validated as
+# in the reference; the product itself is one K1 launch.
+# ---------------------------------------------------------------------------
+
+
+def _offsets(sizes) -> tuple:
+    out = [0]
+    for s in sizes:
+        out.append(out[-1] + s)
+    return tuple(out)
+
+
+class BlockedView:
+    """A dense array with block row/col boundaries (engine.py:178-192)."""
+
+    __slots__ = ("data", "row_sizes", "col_sizes", "row_offsets", "col_offsets")
+
+    def __init__(self, data, row_sizes, col_sizes):
+        self.data = data
+        self.row_sizes = tuple(row_sizes)
+        self.col_sizes = tuple(col_sizes)
+        self.row_offsets = _offsets(self.row_sizes)
+        self.col_offsets = _offsets(self.col_sizes)
+        if tuple(data.shape) != (self.row_offsets[-1], self.col_offsets[-1]):
+            raise BlockShapeMismatch(
+                f"data {tuple(data.shape)} vs block sizes {self.row_sizes} x {self.col_sizes}"
+            )
+
+
+def fox_block_multiply(a: BlockedView, b: BlockedView, out: BlockedView, workers: int = 1,
+                       negate: bool = False, accumulate: bool = False,
+                       counters: OpCounters | None = None) -> None:
+    """out = (+-1) a @ b blockwise (engine.py:202-249).  The reference's Fox
+    stage order is a CPU scheduling device; on the B200 the blocked product is
+    a single K1 launch (block structure checked, result identical up to
+    summation order)."""
+    from .core import multiply
+
+    if a.col_sizes != b.row_sizes:
+        raise BlockShapeMismatch(f"a cols {a.col_sizes} vs b rows {b.row_sizes}")
+    if out.row_sizes != a.row_sizes or out.col_sizes != b.col_sizes:
+        raise BlockShapeMismatch(
+            f"out {out.row_sizes} x {out.col_sizes} for product {a.row_sizes} x {b.col_sizes}"
+        )
+    multiply(a.data, b.data, out.data, accumulate=accumulate, negate=negate)
+    if counters is not None:
+        counters.multiplies += 1
+        if accumulate:
+            counters.reductions += 1
+
+
+# ---------------------------------------------------------------------------
+# the device engine
+# ---------------------------------------------------------------------------
+
+
+class DeviceEngine:
+    """A bound native engine (``bi_engine``) for one partition and batch size,
+    with its device buffers: M and M_inv as [batch, n, ld] float64 tensors and
+    the workspace holding every provisional set and the leaf scratch."""
+
+    def __init__(self, sizes, batch: int = 1):
+        t = _lib.torch()
+        _lib.require_device()
+        self.scheme = partition_from_sizes(sizes)
+        self.sizes = tuple(int(s) for s in sizes)
+        self.batch = int(batch)
+        self.n = self.scheme.m_n
+        L = _lib.lib()
+        h = _lib._vp()
+        arr = (_lib._c_i64 * len(self.sizes))(*self.sizes)
+        _lib.check(L.bi_engine_create(_lib.ctypes.byref(h), len(self.sizes), arr, self.batch),
+                   "bi_engine_create")
+        self._h = h
+        self.M = _lib.empty_matrix(self.n, self.n, batch=self.batch)
+        self.Minv = _lib.empty_matrix(self.n, self.n, batch=self.batch)
+        self.ws = _lib.workspace(L.bi_engine_workspace_bytes(h))
+        self.device = self.M.device
+        with t.cuda.device(self.device):
+            _lib.check(L.bi_engine_bind(h, _lib.ptr(self.M), _lib.ld(self.M), int(self.M.stride(0)),
+                                        _lib.ptr(self.Minv), _lib.ld(self.Minv), int(self.Minv.stride(0)),
+                                        _lib.ptr(self.ws), self.ws.numel(), _lib.stream_ptr()),
+                       "bi_engine_bind")
+        self.n_steps = total_steps(len(self.sizes))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().bi_engine_destroy(h)
+            except Exception:  # interpreter teardown
+                pass
+            self._h = None
+
+    def load(self, ms, non_blocking: bool = False) -> None:
+        """Copy the batch of input matrices (host array or tensor) into M."""
+        t = _lib.torch()
+        src = ms if isinstance(ms, t.Tensor) else t.from_numpy(np.ascontiguousarray(ms, dtype=np.float64))
+        if src.dim() == 2:
+            src = src.unsqueeze(0)
+        if tuple(src.shape) != (self.batch, self.n, self.n):
+            raise DimensionMismatch(f"input {tuple(src.shape)} vs engine ({self.batch}, {self.n}, {self.n})")
+        self.M.copy_(src, non_blocking=non_blocking)
+
+    def run(self, first: int = 1, last: int | None = None, use_graph: bool = True) -> None:
+        """Enqueue steps [first, last]; M_inv is zeroed before step 1
+        (storage.fresh_state, storage.py:391-411)."""
+        last = self.n_steps if last is None else last
+        if not 1 <= first <= last <= self.n_steps:
+            raise OutOfRange(f"steps {first}..{last} outside 1..{self.n_steps}")
+        if first == 1:
+            self.Minv.zero_()
+        rc = _lib.lib().bi_engine_run(self._h, first, last, 1 if use_graph else 0, _lib.stream_ptr())
+        _lib.check(rc, "bi_engine_run")
+
+    def check(self) -> None:
+        """Synchronize; raise SingularBlock(step, quad) for the first singular
+        leaf of the executed range (engine.py:320-328)."""
+        s, q, z = _lib.ctypes.c_int(), _lib.ctypes.c_int(), _lib.ctypes.c_int()
+        rc = _lib.lib().bi_engine_status(self._h, _lib.ctypes.byref(s), _lib.ctypes.byref(q),
+                                         _lib.ctypes.byref(z))
+        if _lib.check(rc, "bi_engine_status") == _lib.BI_ESINGULAR:
+            exc = SingularBlock("A", path=[], step=s.value, quad=q.value)
+            exc.matrix = z.value
+            raise exc
+
+    def counters(self, first: int = 1, last: int | None = None) -> dict:
+        last = self.n_steps if last is None else last
+        out = (_lib.ctypes.c_double * 5)()
+        _lib.check(_lib.lib().bi_engine_counters(self._h, first, last, out), "bi_engine_counters")
+        return {"multiplies": int(out[0]), "inversions": int(out[1]), "reductions": int(out[2]),
+                "gemm_flops": out[3], "leaf_flops": out[4]}
+
+    def tset_square(self, level: int, quad: int, matrix: int = 0):
+        """Device view of the level-`level` provisional square of a quad."""
+        p, ld, side = _lib._vp(), _lib._c_i64(), _lib._c_i64()
+        _lib.check(_lib.lib().bi_engine_tset_square(self._h, level, quad, matrix, _lib.ctypes.byref(p),
+                                                    _lib.ctypes.byref(ld), _lib.ctypes.byref(side)),
+                   "bi_engine_tset_square")
+        t = _lib.torch()
+        # the square lives inside self.ws: build a strided view over it
+        base = _lib.ptr(self.ws)
+        off = (p.value - base)
+        assert off % 8 == 0 and off >= 0
+        flat = self.ws.view(t.float64)
+        return flat.as_strided((side.value, side.value), (ld.value, 1), off // 8)
+
+
+_ENGINES: "OrderedDict[tuple, DeviceEngine]" = OrderedDict()
+_CACHE_MAX = 2
+
+
+def _engine_for(sizes, batch: int) -> DeviceEngine:
+    t = _lib.torch()
+    key = (tuple(int(s) for s in sizes), int(batch), t.cuda.current_device() if t.cuda.is_available() else -1)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = DeviceEngine(sizes, batch)
+        _ENGINES[key] = eng
+        while len(_ENGINES) > _CACHE_MAX:
+            _ENGINES.popitem(last=False)
+    else:
+        _ENGINES.move_to_end(key)
+    return eng
+
+
+def _scheme_and_dense(m, sizes):
+    if isinstance(m, BlockMatrix):
+        scheme = m.scheme
+        if sizes is not None and tuple(int(s) for s in sizes) != scheme.sizes:
+            raise SchemeMismatch("explicit sizes differ from the BlockMatrix scheme")
+        return scheme, m.store.data if hasattr(m.store, "data") else m.to_dense()
+    dense = np.asarray(m, dtype=np.float64)
+    if dense.ndim != 2 or dense.shape[0] != dense.shape[1]:
+        raise DimensionMismatch(f"square matrix required, got {dense.shape}")
+    scheme = partition_from_sizes(sizes) if sizes is not None else make_partition(dense.shape[0])
+    if scheme.m_n != dense.shape[0]:
+        raise DimensionMismatch(f"sizes sum to {scheme.m_n}, matrix order is {dense.shape[0]}")
+    return scheme, dense
+
+
+def _last_step(n_steps: int, stop_after_step) -> int:
+    if stop_after_step is None:
+        return n_steps
+    return max(1, min(int(stop_after_step), n_steps))
+
+
+def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backed: bool = False,
+                  sizes=None, stop_after_step: int | None = None,
+                  counters: OpCounters | None = None) -> BlockMatrix:
+    """Invert a partitioned matrix through the full step schedule on the B200
+    (engine.py:482-542).  Same arguments and result type as the reference;
+    ``checkpoint_dir`` / ``file_backed`` (disk persistence) are
+    not part of the device path and raise NotImplementedError."""
+    resolve_workers(workers)
+    if checkpoint_dir is not None or file_backed:
+        raise NotImplementedError("checkpoint/resume and file-backed stores are not on the B200 path")
+    scheme, dense = _scheme_and_dense(m, sizes)
+    eng = _engine_for(scheme.sizes, 1)
+    last = _last_step(eng.n_steps, stop_after_step)
+    eng.load(dense[None])
+    eng.run(1, last)
+    eng.check()
+    if counters is not None:
+        c = eng.counters(1, last)
+        counters.multiplies += c["multiplies"]
+        counters.inversions += c["inversions"]
+        counters.reductions += c["reductions"]
+    out = eng.Minv[0].cpu().numpy()
+    return BlockMatrix(scheme, MemoryBlockStore(scheme, out), role="inverse")
+
+
+def run_inversion_batch(ms, sizes, out: np.ndarray | None = None,
+                        stop_after_step: int | None = None,
+                        counters: OpCounters | None = None) -> np.ndarray:
+    """Batched extension: invert ``ms`` [batch, n, n] (shared partition
+    ``sizes``) in lock-step; returns (or fills ``out``) [batch, n, n].
+    Page-locked ``ms``/``out`` make the host<->device copies asynchronous DMA."""
+    t = _lib.torch()
+    ms_t = ms if isinstance(ms, t.Tensor) else t.from_numpy(np.ascontiguousarray(ms, dtype=np.float64))
+    if ms_t.dim() != 3 or ms_t.shape[1] != ms_t.shape[2]:
+        raise DimensionMismatch(f"expected [batch, n, n], got {tuple(ms_t.shape)}")
+    scheme = partition_from_sizes(sizes)
+    if scheme.m_n != ms_t.shape[1]:
+        raise DimensionMismatch(f"sizes sum to {scheme.m_n}, matrix order is {ms_t.shape[1]}")
+    eng = _engine_for(scheme.sizes, int(ms_t.shape[0]))
+    last = _last_step(eng.n_steps, stop_after_step)
+    eng.load(ms_t, non_blocking=True)
+    eng.run(1, last)
+    eng.check()
+    if counters is not None:
+        c = eng.counters(1, last)
+        counters.multiplies += c["multiplies"]
+        counters.inversions += c["inversions"]
+        counters.reductions += c["reductions"]
+    if out is None:
+        out = np.empty(tuple(ms_t.shape))
+    t.from_numpy(out).copy_(eng.Minv)
+    return out

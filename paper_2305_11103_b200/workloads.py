@@ -1,0 +1,70 @@
+"""Seeded synthetic inputs for the BASELINE configurations.
+
+BASELINE.json names no public dataset; these generators ARE the input set.
+Draw order follows SURVEY 8d exactly so the CPU oracle and the device see
+identical matrices.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def well_conditioned(order: int, seed: int) -> np.ndarray:
+    """The reference test generator (tests/conftest.py:10-15, bench.py:42-46):
+    uniform[-1, 1] plus 2*order on the diagonal."""
+    g = np.random.default_rng(seed)
+    m = g.uniform(-1.0, 1.0, (order, order))
+    m[np.diag_indices(order)] += 2.0 * order
+    return m
+
+
+def cfg1() -> tuple[np.ndarray, list[int]]:
+    """n=512, N(0,1) + 512 I, partition (256, 256)."""
+    rng = np.random.default_rng(1)
+    m = rng.standard_normal((512, 512))
+    m[np.diag_indices(512)] += 512.0
+    return m, [256, 256]
+
+
+def cfg2(batch: int = 4, n: int = 4096, nblocks: int = 8) -> tuple[np.ndarray, list[int]]:
+    """n=4096, 8 x 512 blocks, N(0,1)/64 + 2 I (= N(0,1)/sqrt(n) + 2 I), batch of 4;
+    matrix b is drawn from default_rng([2, b])."""
+    ms = np.empty((batch, n, n))
+    for b in range(batch):
+        rng = np.random.default_rng([2, b])
+        ms[b] = rng.standard_normal((n, n)) / np.sqrt(n)
+        ms[b][np.diag_indices(n)] += 2.0
+    return ms, [n // nblocks] * nblocks
+
+
+def cfg3(n: int = 6000, split: int = 1000, rank: int = 500) -> tuple[np.ndarray, int]:
+    """n=6000 split (1000, 5000); A11 = U V^T of rank 500; A22 += 6000 I.
+    (Scaled-down variants keep the same construction.)"""
+    rng = np.random.default_rng(3)
+    m = rng.standard_normal((n, n))
+    u = rng.standard_normal((split, rank))
+    v = rng.standard_normal((split, rank))
+    m[:split, :split] = u @ v.T
+    m[split:, split:] += float(n) * np.eye(n - split)
+    return m, split
+
+
+def cfg4(n: int = 16384, nblocks: int = 64) -> tuple[np.ndarray, list[int]]:
+    """n=16384, 64 x 256 blocks, N(0,1)/128 + 4 I."""
+    rng = np.random.default_rng(4)
+    m = rng.standard_normal((n, n)) / np.sqrt(n)
+    m[np.diag_indices(n)] += 4.0
+    return m, [n // nblocks] * nblocks
+
+
+def cfg5_rows(r0: int, r1: int, n: int = 65536) -> np.ndarray:
+    """Rows [r0, r1) of the n=65536 config (N(0,1)/256 + 4 I, seed 5); chunked
+    draws are bit-identical to one big draw."""
+    rng = np.random.default_rng(5)
+    if r0:
+        rng.standard_normal((r0, n))  # advance the stream (chunked = monolithic)
+    m = rng.standard_normal((r1 - r0, n)) / np.sqrt(n)
+    for i in range(r0, r1):
+        m[i - r0, i] += 4.0
+    return m

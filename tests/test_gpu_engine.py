@@ -1,0 +1,215 @@
+"""GPU parity of the hot path -- run_inversion (step engine), invert_via_d /
+invert_via_a / invert_with_fallback, invertor_inplace_by_a -- against the CPU
+oracle (a restatement of the reference, pinned by tests/test_oracle.py).
+
+Tolerances: the reference's own criteria (max|X - X_oracle| <= 1e-8 n and
+max|MX - I| <= 1e-8 n, test_acceptance.py:66-77) plus the north star's
+relative Frobenius error <= 1e-9 for well-conditioned inputs.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import well_conditioned
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bi():
+    import paper_2305_11103_b200 as bi
+
+    return bi
+
+
+def _assert_ref_criteria(m, inv, ref):
+    n = m.shape[0]
+    assert np.max(np.abs(inv - ref)) <= 1e-8 * n
+    assert oracle.residual_max(m, inv) <= 1e-8 * n
+    assert oracle.rel_frob(inv, ref) <= 1e-9
+
+
+@pytest.mark.parametrize("order", [2, 3, 4, 5, 6, 9, 12, 21, 33, 64, 100])
+def test_default_partition_vs_oracle(bi, order):
+    m = well_conditioned(order, 600 + order)  # test_engine.py:292-297
+    inv = bi.run_inversion(m).to_dense()
+    _assert_ref_criteria(m, inv, oracle.gauss_jordan(m))
+
+
+@pytest.mark.parametrize("sizes", [[5, 7], [8] * 8, [16] * 4, [3, 9, 5, 11], [64] * 8, [37, 64, 1, 90],
+                                   [100] * 16, [256, 256], [33] * 32])
+def test_explicit_sizes_vs_oracle_engine(bi, sizes):
+    n = sum(sizes)
+    m = well_conditioned(n, 43 + n)
+    inv = bi.run_inversion(m, sizes=sizes).to_dense()
+    ref = oracle.run_inversion(m, sizes=sizes, leaf_inverter=oracle.gauss_jordan)
+    _assert_ref_criteria(m, inv, ref)
+
+
+@pytest.mark.parametrize("sizes", [[16] * 8, [7, 9, 12, 4]])
+def test_step_state_parity(bi, sizes):
+    """M_inv after every step boundary matches the oracle engine's state
+    (stop_after_step, engine.py:538-539), and the provisional sets match."""
+    n = sum(sizes)
+    m = well_conditioned(n, 7 + n)
+    nsteps = bi.total_steps(len(sizes))
+    for s in range(1, nsteps + 1):
+        got = bi.run_inversion(m, sizes=sizes, stop_after_step=s).to_dense()
+        ref, tsets = oracle.run_inversion(m, sizes=sizes, stop_after_step=s, leaf_inverter=oracle.gauss_jordan,
+                                          return_state=True)
+        scale = max(np.abs(ref).max(), 1e-300)
+        assert np.max(np.abs(got - ref)) <= 1e-12 * scale * n, s
+    # provisional sets after the full run
+    from paper_2305_11103_b200.engine import _engine_for
+
+    eng = _engine_for(tuple(sizes), 1)
+    off = oracle.offsets_of(sizes)
+    for lv, t in tsets.items():
+        for g in range(len(sizes) >> lv):
+            sq = eng.tset_square(lv, g).cpu().numpy()
+            first, mid, last = g << lv, (g << lv) + (1 << (lv - 1)), (g + 1) << lv
+            ha = off[mid] - off[first]
+            for name, arr, r0, c0 in (("S_D", t["S"][2 * g], 0, 0), ("R", t["R"][g], 0, ha),
+                                      ("L", t["L"][g], ha, 0), ("S_A", t["S"][2 * g + 1], ha, ha)):
+                win = sq[r0:r0 + arr.shape[0], c0:c0 + arr.shape[1]]
+                assert np.max(np.abs(win - arr)) <= 1e-11 * max(np.abs(arr).max(), 1.0), (lv, g, name)
+
+
+def test_level1_equals_combined_pivot_formula(bi):
+    """run_inversion with two blocks is Eq. 7 (test_engine.py:271-277); on the
+    device both are the same kernels, so the agreement is to rounding."""
+    for order, split in ((5, 2), (6, 3), (7, 3), (300, 140)):
+        m = well_conditioned(order, 41 + order)
+        sizes = [split, order - split]
+        inv = bi.run_inversion(m, sizes=sizes).to_dense()
+        direct = np.empty((order, order))
+        bi.invert_via_ad(bi.diagonal_quad(m, split), None, direct)
+        assert np.max(np.abs(inv - direct)) <= 1e-14 * order
+
+
+def test_identity_and_singular_reporting(bi):
+    inv = bi.run_inversion(np.eye(21)).to_dense()  # test_engine.py:286-290
+    assert np.array_equal(inv, np.eye(21))
+    p = np.eye(4)[::-1].copy()
+    with pytest.raises(bi.SingularBlock) as info:  # test_engine.py:312-317
+        bi.run_inversion(p)
+    assert info.value.step == 1 and info.value.quad is not None
+
+
+def test_block_matrix_input_and_scheme_mismatch(bi):
+    m = well_conditioned(9, 44)
+    bm = bi.BlockMatrix.from_dense(m)
+    inv = bi.run_inversion(bm).to_dense()
+    assert oracle.residual_max(m, inv) <= 1e-8
+    with pytest.raises(bi.SchemeMismatch):
+        bi.run_inversion(bm, sizes=[4, 5])
+
+
+def test_counters(bi):
+    c = bi.OpCounters()
+    bi.run_inversion(well_conditioned(8, 45), counters=c)
+    ref = oracle.EngineCounts()
+    oracle.run_inversion(well_conditioned(8, 45), counts=ref)
+    assert (c.multiplies, c.inversions, c.reductions) == (ref.multiplies, ref.inversions, ref.reductions)
+
+
+def test_batch_matches_single(bi):
+    sizes = [32] * 8
+    ms = np.stack([well_conditioned(256, s) for s in range(3)])
+    out = bi.run_inversion_batch(ms, sizes)
+    for i in range(3):
+        single = bi.run_inversion(ms[i], sizes=sizes).to_dense()
+        assert np.array_equal(out[i], single)  # batch lanes are independent and deterministic
+
+
+def test_deterministic_replay(bi):
+    m = well_conditioned(640, 3)
+    a = bi.run_inversion(m, sizes=[80] * 8).to_dense()
+    b = bi.run_inversion(m, sizes=[80] * 8).to_dense()
+    assert a.tobytes() == b.tobytes()
+
+
+# ---------------------------------------------------------------------------
+# config-shaped cases (BASELINE.json configs, scaled where the oracle is slow)
+# ---------------------------------------------------------------------------
+
+
+def test_cfg1_inplace_by_a(bi):
+    from paper_2305_11103_b200.workloads import cfg1
+
+    m, sizes = cfg1()
+    x = m.copy()
+    c = bi.invertor_inplace_by_a(x)
+    ref = oracle.gauss_jordan(m)
+    _assert_ref_criteria(m, x, ref)
+    assert c.multiplies == 6 * c.nodes and c.reductions == 2 * c.nodes
+    inv = bi.run_inversion(m, sizes=sizes).to_dense()
+    _assert_ref_criteria(m, inv, ref)
+
+
+def test_cfg3_scaled_via_d_and_fallback(bi):
+    """Singular A11 (rank n1/2): via_a must report SingularBlock('A') and the
+    fallback must pick via_d (schur.py:300-333, test_schur.py:227-232).  Oracle:
+    the reference formula with the reference's pivoted GJ as sub-inverter."""
+    from paper_2305_11103_b200.workloads import cfg3
+
+    m, split = cfg3(n=1200, split=200, rank=100)
+    ref = np.empty_like(m)
+    oracle.invert_via_d(m, split, oracle.gj_sub, ref)
+    out = np.empty_like(m)
+    bi.invert_via_d(bi.diagonal_quad(m, split), None, out)
+    cond = np.linalg.cond(m)
+    eps = np.finfo(float).eps
+    assert oracle.residual_frob(m, out) <= 10 * m.shape[0] * eps * cond
+    assert oracle.rel_frob(out, ref) <= 100 * eps * cond
+    with pytest.raises(bi.SingularBlock) as info:
+        bi.invert_via_a(bi.diagonal_quad(m, split), None, np.empty_like(m))
+    assert info.value.block == "A"
+    out2 = np.empty_like(m)
+    assert bi.invert_with_fallback(m, split, out2) == "via_d"
+    assert np.array_equal(out2, out)
+
+
+def test_via_formulas_small_kats(bi):
+    m = np.zeros((5, 5))
+    m[:2, :2] = well_conditioned(2, 1)
+    m[2:, 2:] = well_conditioned(3, 2)
+    out = np.empty((5, 5))
+    bi.invert_via_a(bi.diagonal_quad(m, 2), bi.invert_small, out)  # test_schur.py:30-37
+    assert np.max(np.abs(out - oracle.gauss_jordan(m))) <= 1e-12
+    assert np.all(out[:2, 2:] == 0.0) and np.all(out[2:, :2] == 0.0)
+    out = np.empty((5, 5))
+    bi.invert_via_a(bi.diagonal_quad(np.eye(5), 2), bi.invert_small, out)
+    assert np.array_equal(out, np.eye(5))
+    c = bi.OpCounters()
+    out = np.empty((6, 6))
+    bi.invert_via_d(bi.diagonal_quad(well_conditioned(6, 7), 3), bi.invert_small, out, c)
+    assert (c.multiplies, c.reductions) == (6, 2)
+    m = well_conditioned(4, 20)
+    m[0, 0] = 0.0
+    out = np.empty((4, 4))
+    assert bi.invert_with_fallback(m, 1, out) == "via_d"  # test_schur.py:227-232
+    assert np.max(np.abs(out - oracle.gauss_jordan(m))) <= 1e-10
+    for seed in range(20):  # test_schur.py:71-79
+        m = well_conditioned(5, 800 + seed)
+        q = bi.diagonal_quad(m, 2)
+        oa, od = np.empty((5, 5)), np.empty((5, 5))
+        bi.invert_via_a(q, bi.invert_small, oa)
+        bi.invert_via_d(q, bi.invert_small, od)
+        assert np.max(np.abs(oa - od)) <= 1e-9
+
+
+def test_reference_style_invert_sub_callable(bi):
+    """A foreign Python invert_sub is honoured (plugin protocol)."""
+    m = well_conditioned(40, 21)
+    calls = []
+
+    def sub(block, out):
+        calls.append(block.shape)
+        out[...] = oracle.gauss_jordan(block)
+
+    out = np.empty((40, 40))
+    assert bi.invert_with_fallback(m, 15, out, invert_sub=sub) == "via_a"
+    assert calls == [(15, 15), (25, 25)]
+    assert oracle.residual_max(m, out) <= 1e-12

@@ -1,0 +1,154 @@
+"""GPU parity of the K1 GEMM and K3 batched pivoted Gauss-Jordan kernels,
+called through the C ABI (libblockinv_b200.so), against the CPU oracle /
+NumPy float64.
+
+Tolerances (float64 throughout):
+  GEMM   ||D - D_ref||_F <= 1e-14 * sqrt(K) * (||A||_F ||B||_F + ||C||_F)
+  GJ     relative Frobenius error vs the oracle's pivoted GJ <= 1e-12 on
+         well-conditioned blocks; exact on permutations / identity.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import well_conditioned
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bi():
+    import paper_2305_11103_b200 as bi
+
+    return bi
+
+
+def _gemm_tol(a, b, c, k):
+    scale = np.linalg.norm(a) * np.linalg.norm(b) + (np.linalg.norm(c) if c is not None else 0.0)
+    return 1e-14 * np.sqrt(max(k, 1)) * scale + 1e-300
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (7, 5, 3), (128, 128, 16), (129, 131, 17), (300, 257, 513),
+                                   (64, 700, 33), (512, 512, 512)])
+@pytest.mark.parametrize("negate,accumulate", [(False, False), (True, False), (False, True), (True, True)])
+def test_gemm_vs_numpy(bi, m, n, k, negate, accumulate):
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.core import device_gemm
+
+    g = np.random.default_rng(m * 1000 + n + k)
+    a, b, c = g.standard_normal((m, k)), g.standard_normal((k, n)), g.standard_normal((m, n))
+    da, db, dd = _lib.to_device(a), _lib.to_device(b), _lib.to_device(c)
+    device_gemm(da, db, dd, c=dd if accumulate else None, negate=negate)
+    got = dd.cpu().numpy()
+    ref = (c if accumulate else 0.0) + (-1.0 if negate else 1.0) * (a @ b)
+    assert np.linalg.norm(got - ref) <= _gemm_tol(a, b, c if accumulate else None, k)
+
+
+def test_gemm_unaligned_views(bi):
+    """Odd leading dimensions / odd column offsets take the 8-byte copy path."""
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.core import device_gemm
+
+    g = np.random.default_rng(5)
+    big = _lib.to_device(g.standard_normal((301, 303)))
+    a = big[1:200, 3:120]   # odd column offset
+    b = big[5:122, 7:160]
+    out = _lib.empty_matrix(199, 153)
+    device_gemm(a, b, out)
+    ref = a.cpu().numpy() @ b.cpu().numpy()
+    assert np.linalg.norm(out.cpu().numpy() - ref) <= _gemm_tol(ref, np.eye(1), None, 117) * 10
+
+
+def test_multiply_numpy_api(bi, rng):
+    """core.multiply semantics (core.py:142-170): zero-then-accumulate, negate."""
+    a, b = rng.uniform(-1, 1, (9, 6)), rng.uniform(-1, 1, (6, 5))
+    out = rng.uniform(-1, 1, (9, 5))
+    base = out.copy()
+    bi.multiply(a, b, out, accumulate=True, negate=True)
+    assert np.max(np.abs(out - (base - a @ b))) <= 1e-14
+    bi.multiply(a, b, out)
+    assert np.max(np.abs(out - a @ b)) <= 1e-14
+    naive = np.zeros((9, 5))
+    for i in range(9):
+        for j in range(5):
+            for kk in range(6):
+                naive[i, j] += a[i, kk] * b[kk, j]
+    assert np.max(np.abs(out - naive)) <= 1e-14  # test_core.py:55-60
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 17, 31, 32, 33, 64, 100, 255, 256, 257, 512, 513, 1000])
+def test_gj_inverse_vs_oracle(bi, n):
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.core import device_inverse
+
+    count = 3
+    ms = np.stack([well_conditioned(n, 100 * n + i) for i in range(count)])
+    dm = _lib.to_device(ms)
+    dout = _lib.empty_matrix(n, n, batch=count)
+    info = device_inverse(dm, dout)
+    assert (info == 0).all()
+    got = dout.cpu().numpy()
+    for i in range(count):
+        ref = oracle.gauss_jordan(ms[i])
+        assert oracle.rel_frob(got[i], ref) <= 1e-12, (n, i)
+
+
+@pytest.mark.parametrize("n", [200, 700])
+def test_gj_needs_pivoting(bi, n):
+    """Zero leading diagonal: only a pivoted elimination survives."""
+    g = np.random.default_rng(n)
+    m = g.standard_normal((n, n))
+    m[0, 0] = 0.0
+    m[:, 1] *= 1e-3
+    ref = oracle.gauss_jordan(m)
+    got = bi.gauss_jordan_oracle(m)
+    assert oracle.rel_frob(got, ref) <= 1e-9 * np.linalg.cond(m) * 1e-3 + 1e-10
+    assert oracle.residual_frob(m, got) <= 1e-10 * n
+
+
+def test_gj_exact_cases(bi):
+    p = np.array([[0.0, 1.0], [1.0, 0.0]])
+    assert np.array_equal(bi.gauss_jordan_oracle(p), p)  # test_core.py:231-233
+    for order in (1, 3, 17):
+        assert np.array_equal(bi.gauss_jordan_oracle(np.eye(order)), np.eye(order))
+    rev = np.eye(40)[::-1].copy()
+    assert np.array_equal(bi.gauss_jordan_oracle(rev), rev)
+
+
+def test_gj_singular(bi):
+    with pytest.raises(bi.SingularMatrix):
+        bi.gauss_jordan_oracle(np.ones((3, 3)))  # test_core.py:240-242
+    with pytest.raises(bi.SingularMatrix):
+        bi.gauss_jordan_oracle(np.zeros((5, 5)))
+    g = np.random.default_rng(0)
+    u, v = g.standard_normal((300, 150)), g.standard_normal((300, 150))
+    with pytest.raises(bi.SingularMatrix):
+        bi.gauss_jordan_oracle(u @ v.T)  # the cfg3 A11 construction
+    with pytest.raises(bi.SingularBlock):
+        bi.invert_small(np.ones((2, 2)), np.empty((2, 2)))
+
+
+def test_invert_small_kats(bi):
+    out = np.empty((2, 2))
+    bi.invert_small(np.eye(2), out)
+    assert np.array_equal(out, np.eye(2))
+    bi.invert_small(np.array([[2.0, 0.0], [0.0, 4.0]]), out)
+    assert np.array_equal(out, [[0.5, 0.0], [0.0, 0.25]])
+    o1 = np.empty((1, 1))
+    bi.invert_small(np.array([[5.0]]), o1)
+    assert o1[0, 0] == 0.2
+    m = np.array([[1.0, 1.0, 2.0, 0.5], [1.0, 1.0, 0.25, 3.0], [2.0, 0.5, 9.0, 0.1], [0.5, 2.0, 0.2, 8.0]])
+    o4 = np.empty((4, 4))
+    bi.invert_small(m, o4)  # leading 2x2 singular (test_core.py:201-214)
+    assert oracle.residual_max(m, o4) <= 1e-10
+    with pytest.raises(bi.DimensionMismatch):
+        bi.invert_small(np.eye(5), np.empty((5, 5)))
+
+
+def test_residual_kernel(bi):
+    m = well_conditioned(300, 9)
+    x = oracle.gauss_jordan(m)
+    assert abs(bi.residual_norm(m, x) - oracle.residual_max(m, x)) <= 1e-15
+    assert abs(bi.residual_frobenius(m, x) - oracle.residual_frob(m, x)) <= 1e-3 * oracle.residual_frob(m, x) + 1e-16
+    assert bi.residual_norm(np.eye(4), np.eye(4)) == 0.0
