@@ -103,6 +103,13 @@ int bi_engine_bind(bi_engine* e,
                    void* workspace, int64_t workspace_bytes, void* stream);
 int bi_engine_run(bi_engine* e, int first_step, int last_step, int use_graph, void* stream);
 int bi_engine_status(bi_engine* e, int* fail_step, int* fail_quad, int* fail_matrix);
+/* Enqueue only one class of ops of steps [first, last] (no graph): mask 1 =
+ * the engine's K1 GEMM launches, 2 = the leaf inversions (K3 incl. their
+ * trailing-update GEMMs), 3 = both.  For per-kernel timing in bench.py. */
+int bi_engine_run_phase(bi_engine* e, int first_step, int last_step, int mask, void* stream);
+/* Kernel launches of steps [first, last]: out[0] total, out[1] K1 (engine
+ * GEMMs + leaf trailing updates), out[2] other K3 kernels. */
+int bi_engine_launches(const bi_engine* e, int first_step, int last_step, int64_t out[3]);
 int bi_engine_counters(const bi_engine* e, int first_step, int last_step, double out[5]);
 /* T-set access for step-state parity: pointer + ld of the level-`level`
  * provisional square of quad `quad` of matrix `matrix` (S_D at A's

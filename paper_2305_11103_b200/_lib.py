@@ -39,6 +39,8 @@ SIGNATURES = [
     ("bi_engine_run", _c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
     ("bi_engine_status", _c_int, [_vp, _pint, _pint, _pint]),
     ("bi_engine_counters", _c_int, [_vp, _c_int, _c_int, _pdbl]),
+    ("bi_engine_run_phase", _c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
+    ("bi_engine_launches", _c_int, [_vp, _c_int, _c_int, ctypes.POINTER(_c_i64)]),
     ("bi_engine_tset_square", _c_int, [_vp, _c_int, _c_int, _c_int, ctypes.POINTER(_vp),
                                        ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)]),
     ("bi_engine_destroy", _c_int, [_vp]),

@@ -480,9 +480,10 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   return 0;
 }
 
-static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s) {
+static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s, int mask = 3) {
   for (int stepid = first; stepid <= last; ++stepid) {
     for (const Op& op : e->step_ops[stepid]) {
+      if (!(mask & (op.kind == 0 ? 2 : 1))) continue;
       cudaError_t err;
       if (op.kind == 0) {
         const InvRec& r = e->invs[op.index];
@@ -529,6 +530,36 @@ extern "C" int bi_engine_run(bi_engine* e, int first_step, int last_step, int us
     it = e->graphs.emplace(key, exec).first;
   }
   BI_CUDA_TRY(cudaGraphLaunch(it->second, s));
+  return 0;
+}
+
+extern "C" int bi_engine_run_phase(bi_engine* e, int first_step, int last_step, int mask, void* stream) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step, "stepid outside 1..N_s");
+  BI_REQUIRE(mask >= 1 && mask <= 3, "mask must be 1 (GEMM ops), 2 (leaf inversions) or 3");
+  e->last_stream = static_cast<cudaStream_t>(stream);
+  BI_CUDA_TRY(enqueue_steps(e, first_step, last_step, e->last_stream, mask));
+  return 0;
+}
+
+extern "C" int bi_engine_launches(const bi_engine* e, int first_step, int last_step, int64_t out[3]) {
+  BI_REQUIRE(e && e->bound && out, "engine not bound");
+  BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps, "stepid outside 1..N_s");
+  int64_t gemm = 0, inv = 0;
+  for (int stepid = first_step; stepid <= last_step; ++stepid)
+    for (const Op& op : e->step_ops[stepid]) {
+      if (op.kind == 1) {
+        gemm += 1;
+      } else {
+        const InvRec& r = e->invs[op.index];
+        const int panels = inv_group_panels(r.g);
+        inv += 2 + panels;                       // load + panels + store
+        gemm += (r.g.n > 32) ? panels : 0;       // trailing updates (K1)
+      }
+    }
+  out[0] = gemm + inv;
+  out[1] = gemm;
+  out[2] = inv;
   return 0;
 }
 

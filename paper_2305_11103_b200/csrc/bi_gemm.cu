@@ -166,43 +166,59 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_con
   }
 
   // ---- epilogue: D = [C] + sign * acc, with the optional column remap ----
+  // All C loads are issued before any D store (C may alias D, so the
+  // compiler cannot reorder them itself; interleaving would serialize one
+  // DRAM round trip per fragment).
   const double* C = d.C ? d.C + bz * d.sC : nullptr;
   double* D = d.D + bz * d.sD;
   const int64_t ldc = d.ldc, ldd = d.ldd;
   const double sgn = d.neg ? -1.0 : 1.0;
+  const int skip_at = d.skip_at, skip_len = d.skip_len;
+  auto pcol = [&](int g) { return g < skip_at ? g : g + skip_len; };
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      acc[i][j][0] *= sgn;
+      acc[i][j][1] *= sgn;
+    }
+  if (C) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = wm * 64 + i * 8 + fr;
+      const int64_t row = m0 + r;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cl = wn * 32 + j * 8 + 2 * fc;
+        if (r >= mrem || cl >= nrem) continue;
+        const int p0 = pcol(n0 + cl), p1 = pcol(n0 + cl + 1);
+        const double* cp = C + row * ldc + p0;
+        if (cl + 1 < nrem && p1 == p0 + 1 && (((uintptr_t)cp) & 15) == 0) {
+          const double2 cv = __ldg(reinterpret_cast<const double2*>(cp));
+          acc[i][j][0] += cv.x;
+          acc[i][j][1] += cv.y;
+        } else {
+          acc[i][j][0] += cp[0];
+          if (cl + 1 < nrem) acc[i][j][1] += C[row * ldc + p1];
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = wm * 64 + i * 8 + fr;
-    if (r >= mrem) continue;
     const int64_t row = m0 + r;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int cl = wn * 32 + j * 8 + 2 * fc;
-      if (cl >= nrem) continue;
-      const int g0 = n0 + cl;
-      const int p0 = g0 < d.skip_at ? g0 : g0 + d.skip_len;
-      const int g1 = g0 + 1;
-      const int p1 = g1 < d.skip_at ? g1 : g1 + d.skip_len;
-      const bool two = (cl + 1) < nrem;
-      double v0 = sgn * acc[i][j][0], v1 = sgn * acc[i][j][1];
+      if (r >= mrem || cl >= nrem) continue;
+      const int p0 = pcol(n0 + cl), p1 = pcol(n0 + cl + 1);
       double* dp = D + row * ldd + p0;
-      const double* cp = C ? C + row * ldc + p0 : nullptr;
-      const bool vec = two && p1 == p0 + 1 && ((((uintptr_t)dp) | (cp ? (uintptr_t)cp : 0)) & 15) == 0;
-      if (vec) {
-        if (cp) {
-          const double2 cv = *reinterpret_cast<const double2*>(cp);
-          v0 += cv.x;
-          v1 += cv.y;
-        }
-        *reinterpret_cast<double2*>(dp) = make_double2(v0, v1);
+      if (cl + 1 < nrem && p1 == p0 + 1 && (((uintptr_t)dp) & 15) == 0) {
+        *reinterpret_cast<double2*>(dp) = make_double2(acc[i][j][0], acc[i][j][1]);
       } else {
-        if (cp) v0 += cp[0];
-        dp[0] = v0;
-        if (two) {
-          double* dq = D + row * ldd + p1;
-          if (C) v1 += C[row * ldc + p1];
-          dq[0] = v1;
-        }
+        dp[0] = acc[i][j][0];
+        if (cl + 1 < nrem) D[row * ldd + p1] = acc[i][j][1];
       }
     }
   }

@@ -248,6 +248,19 @@ class DeviceEngine:
         rc = _lib.lib().bi_engine_run(self._h, first, last, 1 if use_graph else 0, _lib.stream_ptr())
         _lib.check(rc, "bi_engine_run")
 
+    def run_phase(self, mask: int, first: int = 1, last: int | None = None) -> None:
+        """Enqueue only the K1 GEMM ops (mask 1) or only the leaf inversions
+        (mask 2) of steps [first, last] -- per-kernel timing for the roofline."""
+        last = self.n_steps if last is None else last
+        _lib.check(_lib.lib().bi_engine_run_phase(self._h, first, last, mask, _lib.stream_ptr()),
+                   "bi_engine_run_phase")
+
+    def launches(self, first: int = 1, last: int | None = None) -> dict:
+        last = self.n_steps if last is None else last
+        out = (_lib._c_i64 * 3)()
+        _lib.check(_lib.lib().bi_engine_launches(self._h, first, last, out), "bi_engine_launches")
+        return {"total": int(out[0]), "gemm": int(out[1]), "inversion": int(out[2])}
+
     def check(self) -> None:
         """Synchronize; raise SingularBlock(step, quad) for the first singular
         leaf of the executed range (engine.py:320-328)."""
