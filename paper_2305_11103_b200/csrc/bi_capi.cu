@@ -90,8 +90,6 @@ cudaError_t launch_residual(int64_t n, int batch, const double* a, int64_t lda, 
   return cudaSuccess;
 }
 
-cudaError_t inv_init_attributes_public();
-
 cudaError_t init_attributes() {
   cudaError_t e = gemm_init_attributes();
   if (e == cudaSuccess) e = inv_init_attributes_public();
@@ -138,7 +136,7 @@ static cudaError_t inv1(int64_t n, const double* src, int64_t lds, double* dst, 
   g.ld_dst = ldd;
   inv_group_layout(g, scratch);
   g.info = info;
-  return launch_inv_group(g, nullptr, s);
+  return launch_inv_group(g, s);
 }
 
 }  // namespace bi
@@ -198,7 +196,7 @@ extern "C" int bi_inv_batched(int count, int64_t n, const double* in, int64_t ld
   g.ld_dst = ld_out;
   inv_group_layout(g, workspace);
   g.info = info;
-  BI_CUDA_TRY(launch_inv_group(g, nullptr, static_cast<cudaStream_t>(stream)));
+  BI_CUDA_TRY(launch_inv_group(g, static_cast<cudaStream_t>(stream)));
   return 0;
 }
 

@@ -95,7 +95,7 @@ struct InvGroup {
   // scratch (device), laid out by inv_group_layout
   double* W;        // count * n * ldw
   int64_t ldw;
-  double* tmp;      // count * 32 * ldw
+  double* tmp;      // count * 128 * ldw
   int* perm;        // count * n
   int* flags;       // count * n
   unsigned long long* maxabs;  // count (bit pattern of max|.|)
@@ -105,15 +105,11 @@ struct InvGroup {
 int64_t inv_group_scratch_bytes(int n, int count);
 // Assign scratch pointers from `base` (needs inv_group_scratch_bytes bytes).
 void inv_group_layout(InvGroup& g, void* base);
-// Number of panels and the per-panel trailing-update descriptors (host);
-// descriptors are strided over the group's workspace slab.
-int inv_group_panels(const InvGroup& g);
-void inv_group_panel_desc(const InvGroup& g, int panel, GemmDesc* out);
-// Full inversion of the group on `stream`: init, load, panels (+updates), store.
-// `d_panel_descs`: optional device copy of the panel descriptors (count = panels);
-// when null, descriptors go inline in the kernel parameters.
-cudaError_t launch_inv_group(const InvGroup& g, const GemmDesc* d_panel_descs,
-                             cudaStream_t stream);
+// Kernel launches (total incl. K1 updates) and K1 launches of one group.
+void inv_group_launch_counts(const InvGroup& g, int64_t* kernels, int64_t* gemms);
+// Full inversion of the group on `stream`: init, load, panels + updates, store.
+cudaError_t launch_inv_group(const InvGroup& g, cudaStream_t stream);
+cudaError_t inv_init_attributes_public();
 
 // ---------------------------------------------------------------------------
 // K4 residual
@@ -121,6 +117,50 @@ cudaError_t launch_inv_group(const InvGroup& g, const GemmDesc* d_panel_descs,
 cudaError_t launch_residual(int64_t n, int batch, const double* a, int64_t lda, int64_t sa,
                             const double* x, int64_t ldx, int64_t sx, double* out,
                             double* scratch, cudaStream_t stream);
+
+// Launch priority applied to every kernel the calling thread launches
+// (cudaLaunchAttributePriority; 0 = default).  The engine raises it around
+// the latency-bound leaf inversions so their CTAs win freed SMs from the
+// throughput-bound GEMMs of the other lane.
+extern thread_local int g_launch_priority;
+struct PriorityScope {
+  int saved;
+  explicit PriorityScope(int p) : saved(g_launch_priority) { g_launch_priority = p; }
+  ~PriorityScope() { g_launch_priority = saved; }
+};
+int high_launch_priority();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                             unsigned cluster, bool force_cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  unsigned na = 0;
+  if (cluster > 1 || force_cluster) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (g_launch_priority != 0) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na].val.priority = g_launch_priority;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                          unsigned cluster, Args&&... args) {
+  return launch_kernel_ex(kernel, grid, block, smem, stream, cluster, false, static_cast<Args&&>(args)...);
+}
 
 // Set kernel attributes (dynamic smem, cluster sizes) once per process.
 cudaError_t init_attributes();

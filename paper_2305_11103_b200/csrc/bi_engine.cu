@@ -20,6 +20,7 @@
 //  * singular leaves are recorded per diag step on the device and resolved
 //    to (step, quad, matrix) after the range (no host syncs inside it).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -120,11 +121,11 @@ struct GemmLaunchRec {
 
 struct InvRec {
   InvGroup g;           // device pointers filled at bind
-  int panel_first;      // into descriptor table (per-panel update descs)
   int diag_step_index;  // which diag step (for info reporting)
   std::vector<int> item_block;   // block index p of each item
   std::vector<int> item_matrix;  // matrix index z of each item
   int info_offset;      // into the info region (ints)
+  int lane;             // which lane (scratch region / stream)
 };
 
 struct Window {
@@ -153,12 +154,16 @@ struct bi_engine {
   int64_t t_matrix = 0;              // elements per matrix (all levels)
   int64_t t_bytes = 0, inv_scratch = 0, info_ints = 0, meta_bytes = 0;
   double* T = nullptr;
-  void* inv_base = nullptr;
+  static constexpr int kMaxLanes = 8;
+  void* inv_base[kMaxLanes] = {};
+  int nlanes = 1;
+  int leaf_priority = 0;
+  int zlo[kMaxLanes] = {}, zhi[kMaxLanes] = {};
   int* info = nullptr;
   GemmDesc* d_descs = nullptr;
   void* d_ptrs = nullptr;
   // schedule
-  std::vector<std::vector<Op>> step_ops;  // [stepid]
+  std::vector<std::vector<Op>> lane_ops[kMaxLanes];  // [lane][stepid]
   std::vector<GemmDesc> descs;            // host copy of the table
   std::vector<GemmLaunchRec> launches;
   std::vector<InvRec> invs;
@@ -166,6 +171,8 @@ struct bi_engine {
   bool bound = false;
   cudaStream_t last_stream = nullptr;
   cudaStream_t capture_stream = nullptr;
+  cudaStream_t aux_stream[kMaxLanes] = {};  // lanes 1.. (lane 0 runs on the caller's stream)
+  cudaEvent_t ev_fork = nullptr, ev_skew[kMaxLanes] = {}, ev_join[kMaxLanes] = {};
   std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
   int last_first = 1, last_last = 0;
 
@@ -175,6 +182,12 @@ struct bi_engine {
   ~bi_engine() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (capture_stream) cudaStreamDestroy(capture_stream);
+    for (int l = 0; l < kMaxLanes; ++l) {
+      if (aux_stream[l]) cudaStreamDestroy(aux_stream[l]);
+      if (ev_skew[l]) cudaEventDestroy(ev_skew[l]);
+      if (ev_join[l]) cudaEventDestroy(ev_join[l]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
     if (meta_dev) cudaFree(meta_dev);
   }
 
@@ -235,9 +248,22 @@ extern "C" int bi_engine_create(bi_engine** out, int nblocks, const int64_t* siz
   }
   e->t_matrix = t;
   e->t_bytes = align256(t * 8 * (int64_t)batch);
-  // leaf scratch: the largest equal-size group of one diag step
+  // Lanes: with >= 2 matrices the batch is split in two halves that run on two
+  // streams, lane 1 one step behind lane 0, so latency-bound leaf steps of
+  // one lane overlap GEMM-bound steps of the other (BI_ENGINE_LANES=1 disables).
+  const char* lanes_env = getenv("BI_ENGINE_LANES");
+  int want = lanes_env ? atoi(lanes_env) : bi_engine::kMaxLanes;
+  want = std::max(1, std::min(want, bi_engine::kMaxLanes));
+  e->nlanes = std::min(want, batch);
+  for (int l = 0; l < e->nlanes; ++l) {  // contiguous, near-equal matrix ranges
+    e->zlo[l] = (int)((int64_t)batch * l / e->nlanes);
+    e->zhi[l] = (int)((int64_t)batch * (l + 1) / e->nlanes);
+  }
+  // leaf scratch (per lane): the largest equal-size group of one diag step
   std::map<int64_t, int> cnt;
-  for (int64_t s : e->sizes) cnt[s] += batch;
+  int lane_max = 0;
+  for (int l = 0; l < e->nlanes; ++l) lane_max = std::max(lane_max, e->zhi[l] - e->zlo[l]);
+  for (int64_t s : e->sizes) cnt[s] += lane_max;
   int64_t scratch = 0;
   for (auto& kv : cnt) scratch = std::max(scratch, inv_group_scratch_bytes((int)kv.first, kv.second));
   e->inv_scratch = align256(scratch);
@@ -250,16 +276,16 @@ extern "C" int bi_engine_create(bi_engine** out, int nblocks, const int64_t* siz
 extern "C" int64_t bi_engine_workspace_bytes(const bi_engine* e) {
   if (!e) return -1;
   // schedule metadata (descriptor and pointer tables) is engine-owned device memory
-  return e->t_bytes + e->inv_scratch + align256(e->info_ints * 4);
+  return e->t_bytes + e->nlanes * e->inv_scratch + align256(e->info_ints * 4);
 }
 
 static int build_schedule(bi_engine* e) {
-  e->step_ops.assign(e->nsteps + 1, {});
+  for (int l = 0; l < bi_engine::kMaxLanes; ++l) e->lane_ops[l].assign(e->nsteps + 1, {});
   e->descs.clear();
   e->launches.clear();
   e->invs.clear();
   e->diag_steps.clear();
-  const int nb = e->nb, Z = e->Z;
+  const int nb = e->nb;
   const auto& off = e->off;
   auto add_launch = [&](const std::vector<GemmDesc>& raw) -> int {
     std::vector<GemmDesc> m = merge_descs(raw);
@@ -289,38 +315,44 @@ static int build_schedule(bi_engine* e) {
     g.skip_len = 0;
     return g;
   };
-  int diag_index = 0;
   int info_cursor = 0;
   for (int stepid = 1; stepid <= e->nsteps; ++stepid) {
     StepAct a;
     loopid_decode(stepid, nb, &a);
-    auto& ops = e->step_ops[stepid];
+    if (a.kind == 0 || a.kind == 2) e->diag_steps.push_back(stepid);
+  }
+  for (int lane = 0; lane < e->nlanes; ++lane) {
+  const int Z0 = e->zlo[lane], Z1 = e->zhi[lane];
+  int diag_index = 0;
+  for (int stepid = 1; stepid <= e->nsteps; ++stepid) {
+    StepAct a;
+    loopid_decode(stepid, nb, &a);
+    auto& ops = e->lane_ops[lane][stepid];
     if (a.kind == 0 || a.kind == 2) {
       // diag: group leaves (z, p) by block size
       std::map<int64_t, std::vector<std::pair<int, int>>> groups;
-      for (int z = 0; z < Z; ++z)
+      for (int z = Z0; z < Z1; ++z)
         for (int p = 0; p < nb; ++p) groups[e->sizes[p]].push_back({z, p});
       for (auto& kv : groups) {
         InvRec r{};
         r.g.n = (int)kv.first;
         r.g.count = (int)kv.second.size();
         r.diag_step_index = diag_index;
+        r.lane = lane;
         r.info_offset = info_cursor;
         info_cursor += r.g.count;
         for (auto& zp : kv.second) {
           r.item_matrix.push_back(zp.first);
           r.item_block.push_back(zp.second);
         }
-        r.panel_first = -1;
         e->invs.push_back(std::move(r));
         ops.push_back({0, (int)e->invs.size() - 1});
       }
-      e->diag_steps.push_back(stepid);
       ++diag_index;
       if (a.kind == 2) {
         for (int lv = 1; lv <= a.depth; ++lv) {
           std::vector<GemmDesc> raw;
-          for (int z = 0; z < Z; ++z)
+          for (int z = Z0; z < Z1; ++z)
             for (int g = 0; g < (nb >> lv); ++g) {
               const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
               const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
@@ -328,7 +360,7 @@ static int build_schedule(bi_engine* e) {
               raw.push_back(gemm(e->tset_window(lv, z, mid, last, first, mid), e->minv_window(z, first, first),
                                  nullptr, 0, e->minv_window(z, mid, first), hd, ha, ha, 0));
             }
-          for (int z = 0; z < Z; ++z)
+          for (int z = Z0; z < Z1; ++z)
             for (int g = 0; g < (nb >> lv); ++g) {
               const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
               const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
@@ -343,7 +375,7 @@ static int build_schedule(bi_engine* e) {
       const int lv = a.sid;
       std::vector<GemmDesc> l1, l2;
       for (int kind = 0; kind < 2; ++kind)
-        for (int z = 0; z < Z; ++z)
+        for (int z = Z0; z < Z1; ++z)
           for (int g = 0; g < (nb >> lv); ++g) {
             const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
             const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
@@ -358,7 +390,7 @@ static int build_schedule(bi_engine* e) {
             }
           }
       for (int kind = 0; kind < 2; ++kind)
-        for (int z = 0; z < Z; ++z)
+        for (int z = Z0; z < Z1; ++z)
           for (int g = 0; g < (nb >> lv); ++g) {
             const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
             const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
@@ -379,6 +411,7 @@ static int build_schedule(bi_engine* e) {
       ops.push_back({1, add_launch(l1)});
       ops.push_back({1, add_launch(l2)});
     }
+  }
   }
   return 0;
 }
@@ -403,11 +436,25 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   char* p = e->ws;
   e->T = reinterpret_cast<double*>(p);
   p += e->t_bytes;
-  e->inv_base = p;
-  p += e->inv_scratch;
+  for (int l = 0; l < e->nlanes; ++l) {
+    e->inv_base[l] = p;
+    p += e->inv_scratch;
+  }
   e->info = reinterpret_cast<int*>(p);
   p += align256(e->info_ints * 4);
   BI_CUDA_TRY(init_attributes());
+  {
+    const char* pe = getenv("BI_LEAF_PRIORITY");
+    e->leaf_priority = (pe && atoi(pe) == 0) ? 0 : high_launch_priority();
+  }
+  if (e->nlanes > 1 && !e->ev_fork) {
+    BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+    for (int l = 0; l < e->nlanes; ++l) {
+      if (l > 0) BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->aux_stream[l], cudaStreamNonBlocking));
+      BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_skew[l], cudaEventDisableTiming));
+      BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_join[l], cudaEventDisableTiming));
+    }
+  }
 
   int rc = build_schedule(e);
   if (rc) return rc;
@@ -424,15 +471,8 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   };
   std::vector<PtrTab> tabs;
   for (InvRec& r : e->invs) {
-    inv_group_layout(r.g, e->inv_base);
+    inv_group_layout(r.g, e->inv_base[r.lane]);
     r.g.info = e->info + r.info_offset;
-    const int panels = inv_group_panels(r.g);
-    r.panel_first = (int)e->descs.size();
-    for (int pnl = 0; pnl < panels; ++pnl) {
-      GemmDesc d;
-      inv_group_panel_desc(r.g, pnl, &d);
-      e->descs.push_back(d);
-    }
     tabs.push_back({reserve(r.g.count * 8), reserve(r.g.count * 8), reserve(r.g.count * 8),
                     reserve(r.g.count * 8)});
   }
@@ -480,22 +520,45 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   return 0;
 }
 
-static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s, int mask = 3) {
+static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cudaStream_t s, int mask,
+                                cudaEvent_t after_first = nullptr) {
   for (int stepid = first; stepid <= last; ++stepid) {
-    for (const Op& op : e->step_ops[stepid]) {
+    for (const Op& op : e->lane_ops[lane][stepid]) {
       if (!(mask & (op.kind == 0 ? 2 : 1))) continue;
       cudaError_t err;
       if (op.kind == 0) {
-        const InvRec& r = e->invs[op.index];
-        err = launch_inv_group(r.g, e->d_descs + r.panel_first, s);
+        PriorityScope ps(e->leaf_priority);
+        err = launch_inv_group(e->invs[op.index].g, s);
       } else {
         const GemmLaunchRec& L = e->launches[op.index];
         err = launch_gemm(e->descs.data() + L.first, e->d_descs + L.first, L.count, s);
       }
       if (err != cudaSuccess) return err;
     }
+    if (after_first && stepid == first) {
+      cudaError_t err = cudaEventRecord(after_first, s);
+      if (err != cudaSuccess) return err;
+    }
   }
   return cudaSuccess;
+}
+
+static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s, int mask = 3) {
+  if (e->nlanes == 1) return enqueue_lane(e, 0, first, last, s, mask);
+  // Lanes: lane l runs on its own stream, starting after lane l-1 completes
+  // its first step (a one-step skew per lane); all lanes join back into `s`.
+  cudaError_t err = cudaEventRecord(e->ev_fork, s);
+  for (int l = 0; l < e->nlanes && err == cudaSuccess; ++l) {
+    cudaStream_t ls = l == 0 ? s : e->aux_stream[l];
+    if (l > 0) {
+      err = cudaStreamWaitEvent(ls, e->ev_fork, 0);
+      if (err == cudaSuccess) err = cudaStreamWaitEvent(ls, e->ev_skew[l - 1], 0);
+    }
+    if (err == cudaSuccess) err = enqueue_lane(e, l, first, last, ls, mask, e->ev_skew[l]);
+    if (err == cudaSuccess && l > 0) err = cudaEventRecord(e->ev_join[l], ls);
+  }
+  for (int l = 1; l < e->nlanes && err == cudaSuccess; ++l) err = cudaStreamWaitEvent(s, e->ev_join[l], 0);
+  return err;
 }
 
 extern "C" int bi_engine_run(bi_engine* e, int first_step, int last_step, int use_graph, void* stream) {
@@ -546,15 +609,17 @@ extern "C" int bi_engine_launches(const bi_engine* e, int first_step, int last_s
   BI_REQUIRE(e && e->bound && out, "engine not bound");
   BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps, "stepid outside 1..N_s");
   int64_t gemm = 0, inv = 0;
+  for (int lane = 0; lane < e->nlanes; ++lane)
   for (int stepid = first_step; stepid <= last_step; ++stepid)
-    for (const Op& op : e->step_ops[stepid]) {
+    for (const Op& op : e->lane_ops[lane][stepid]) {
       if (op.kind == 1) {
         gemm += 1;
       } else {
         const InvRec& r = e->invs[op.index];
-        const int panels = inv_group_panels(r.g);
-        inv += 2 + panels;                       // load + panels + store
-        gemm += (r.g.n > 32) ? panels : 0;       // trailing updates (K1)
+        int64_t k = 0, gm = 0;
+        inv_group_launch_counts(r.g, &k, &gm);
+        inv += k - gm;
+        gemm += gm;
       }
     }
   out[0] = gemm + inv;

@@ -17,18 +17,38 @@
 #include "bi_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace bi {
+
+thread_local int g_launch_priority = 0;
+
+int high_launch_priority() {
+  static int prio = [] {
+    int least = 0, greatest = 0;
+    if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
+    return greatest;
+  }();
+  return prio;
+}
+
 namespace {
 
-constexpr int kStages = 4;
-constexpr int kThreads = 256;
-constexpr int kALd = kBK + 4;  // 20 doubles: A tile stored [m][k]
-constexpr int kBLd = kBN + 4;  // 132 doubles: B tile stored [k][n]
-constexpr int kAStage = kBM * kALd;
-constexpr int kBStage = kBK * kBLd;
-constexpr int kSmemBytes = kStages * (kAStage + kBStage) * (int)sizeof(double);
+// Kernel configuration: WMW x WNW warps, each owning a WTM x WTN accumulator
+// tile; CTA tile kBM x kBN (128 x 128); BK-deep k-tiles, STAGES-deep ring.
+template <int WMW, int WNW, int WTM, int WTN, int BK, int STAGES>
+struct Cfg {
+  static constexpr int kThreads = WMW * WNW * 32;
+  static constexpr int kFM = WTM / 8, kFN = WTN / 8;  // 8x8 DMMA fragments per warp
+  static constexpr int kALd = BK + 4;   // A tile stored [m][k] (pad 4: conflict-free fragment loads)
+  static constexpr int kBLd = kBN + 4;  // B tile stored [k][n]
+  static constexpr int kAStage = kBM * kALd;
+  static constexpr int kBStage = BK * kBLd;
+  static constexpr int kSmem = STAGES * (kAStage + kBStage) * (int)sizeof(double);
+  static_assert(WMW * WTM == kBM && WNW * WTN == kBN, "CTA tile must be 128 x 128");
+  static_assert(kSmem <= 227 * 1024, "shared memory");
+};
 
 __device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int src_bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -50,10 +70,14 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
+template <int WMW, int WNW, int WTM, int WTN, int BK, int STAGES>
+__global__ void __launch_bounds__(WMW* WNW * 32, 1) gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
+  using C_ = Cfg<WMW, WNW, WTM, WTN, BK, STAGES>;
+  constexpr int kThreads = C_::kThreads, kFM = C_::kFM, kFN = C_::kFN;
+  constexpr int kALd = C_::kALd, kBLd = C_::kBLd, kAStage = C_::kAStage, kBStage = C_::kBStage;
   extern __shared__ __align__(128) double smem[];
   double* sA = smem;
-  double* sB = smem + kStages * kAStage;
+  double* sB = smem + STAGES * kAStage;
 
   // ---- locate this CTA's (descriptor, batch item, tile) -------------------
   const int tile = blockIdx.x;
@@ -78,15 +102,46 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_con
   const bool al16 = ((((uintptr_t)A) | ((uintptr_t)B)) & 15) == 0 && ((lda | ldb) & 1) == 0;
 
   const int tid = threadIdx.x;
+  // Interior tiles with aligned operands take the fast path: per-thread copy
+  // pointers are computed once and advanced by BK per k-tile, no bounds checks.
+  constexpr int kAChunks = (kBM * BK / 2) / kThreads, kBChunks = (BK * kBN / 2) / kThreads;
+  constexpr int kAChunksRow = BK / 2, kBChunksRow = kBN / 2;
+  const bool fast = al16 && mrem >= kBM && nrem >= kBN && (K % BK) == 0;
+  const double* a_src[kAChunks];
+  const double* b_src[kBChunks];
+  int a_dst[kAChunks], b_dst[kBChunks];
+#pragma unroll
+  for (int i = 0; i < kAChunks; ++i) {
+    const int q = tid + i * kThreads, row = q / kAChunksRow, cc = q % kAChunksRow;
+    a_src[i] = A + (int64_t)row * lda + 2 * cc;
+    a_dst[i] = row * kALd + 2 * cc;
+  }
+#pragma unroll
+  for (int i = 0; i < kBChunks; ++i) {
+    const int q = tid + i * kThreads, row = q / kBChunksRow, cc = q % kBChunksRow;
+    b_src[i] = B + (int64_t)row * ldb + 2 * cc;
+    b_dst[i] = row * kBLd + 2 * cc;
+  }
+  const int64_t b_step = (int64_t)BK * ldb;
+  auto load_a_fast = [&](int stage, int kt) {
+    double* as = sA + stage * kAStage;
+#pragma unroll
+    for (int i = 0; i < kAChunks; ++i) cp_async16(as + a_dst[i], a_src[i] + kt * BK, 16);
+  };
+  auto load_b_fast = [&](int stage, int kt) {
+    double* bs = sB + stage * kBStage;
+#pragma unroll
+    for (int i = 0; i < kBChunks; ++i) cp_async16(bs + b_dst[i], b_src[i] + kt * b_step, 16);
+  };
   auto load_stage = [&](int stage, int kt) {
-    const int k0 = kt * kBK;
+    const int k0 = kt * BK;
     double* as = sA + stage * kAStage;
     double* bs = sB + stage * kBStage;
     if (al16) {
 #pragma unroll
-      for (int i = 0; i < (kBM * kBK / 2) / kThreads; ++i) {  // A: 128 rows x 8 chunks
+      for (int i = 0; i < kAChunks; ++i) {
         const int q = tid + i * kThreads;
-        const int row = q >> 3, cc = q & 7, kk = k0 + 2 * cc;
+        const int row = q / kAChunksRow, cc = q % kAChunksRow, kk = k0 + 2 * cc;
         int bytes = 0;
         const double* src = A;
         if (row < mrem && kk < K) {
@@ -96,9 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_con
         cp_async16(as + row * kALd + 2 * cc, src, bytes);
       }
 #pragma unroll
-      for (int i = 0; i < (kBK * kBN / 2) / kThreads; ++i) {  // B: 16 rows x 64 chunks
+      for (int i = 0; i < kBChunks; ++i) {
         const int q = tid + i * kThreads;
-        const int row = q >> 6, cc = q & 63, kk = k0 + row;
+        const int row = q / kBChunksRow, cc = q % kBChunksRow, kk = k0 + row;
         int bytes = 0;
         const double* src = B;
         if (kk < K && 2 * cc < nrem) {
@@ -109,16 +164,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_con
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < (kBM * kBK) / kThreads; ++i) {
+      for (int i = 0; i < (kBM * BK) / kThreads; ++i) {
         const int q = tid + i * kThreads;
-        const int row = q >> 4, kc = q & 15, kk = k0 + kc;
+        const int row = q / BK, kc = q % BK, kk = k0 + kc;
         const bool ok = row < mrem && kk < K;
         cp_async8(as + row * kALd + kc, ok ? A + (int64_t)row * lda + kk : A, ok ? 8 : 0);
       }
 #pragma unroll
-      for (int i = 0; i < (kBK * kBN) / kThreads; ++i) {
+      for (int i = 0; i < (BK * kBN) / kThreads; ++i) {
         const int q = tid + i * kThreads;
-        const int row = q >> 7, nc = q & 127, kk = k0 + row;
+        const int row = q / kBN, nc = q % kBN, kk = k0 + row;
         const bool ok = kk < K && nc < nrem;
         cp_async8(bs + row * kBLd + nc, ok ? B + (int64_t)kk * ldb + nc : B, ok ? 8 : 0);
       }
@@ -126,43 +181,55 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_con
   };
 
   const int warp = tid >> 5, lane = tid & 31;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
+  const int wm = warp / WNW, wn = warp % WNW;
   const int fr = lane >> 2, fc = lane & 3;
 
-  double acc[8][4][2];
+  double acc[kFM][kFN][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < kFM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < kFN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int KT = (K + kBK - 1) / kBK;
+  const int KT = (K + BK - 1) / BK;
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
-    if (s < KT) load_stage(s, s);
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) {
+      if (fast) {
+        load_a_fast(s, s);
+        load_b_fast(s, s);
+      } else {
+        load_stage(s, s);
+      }
+    }
     cp_async_commit();
   }
   for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<kStages - 2>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
-      const int nk = kt + kStages - 1;
-      if (nk < KT) load_stage(nk % kStages, nk);
-      cp_async_commit();
+    const int nk = kt + STAGES - 1;
+    const bool pre = nk < KT;
+    const int nstage = nk % STAGES;
+    const double* as = sA + (kt % STAGES) * kAStage + (wm * WTM + fr) * kALd + fc;
+    const double* bs = sB + (kt % STAGES) * kBStage + fc * kBLd + wn * WTN + fr;
+    if (pre && !fast) load_stage(nstage, nk);
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      double af[kFM], bf[kFN];
+#pragma unroll
+      for (int i = 0; i < kFM; ++i) af[i] = as[i * 8 * kALd + ks * 4];
+#pragma unroll
+      for (int j = 0; j < kFN; ++j) bf[j] = bs[ks * 4 * kBLd + j * 8];
+#pragma unroll
+      for (int i = 0; i < kFM; ++i)
+#pragma unroll
+        for (int j = 0; j < kFN; ++j) dmma(acc[i][j], af[i], bf[j]);
+      // spread the next stage's copies between k-steps (fast path)
+      if (fast && pre) {
+        if (ks == 0) load_a_fast(nstage, nk);
+        if (ks == 1) load_b_fast(nstage, nk);
+      }
     }
-    const double* as = sA + (kt % kStages) * kAStage + (wm * 64 + fr) * kALd + fc;
-    const double* bs = sB + (kt % kStages) * kBStage + fc * kBLd + wn * 32 + fr;
-#pragma unroll
-    for (int ks = 0; ks < kBK / 4; ++ks) {
-      double af[8], bf[4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) af[i] = as[i * 8 * kALd + ks * 4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = bs[ks * 4 * kBLd + j * 8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
-    }
+    cp_async_commit();
   }
 
   // ---- epilogue: D = [C] + sign * acc, with the optional column remap ----
@@ -176,20 +243,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_con
   const int skip_at = d.skip_at, skip_len = d.skip_len;
   auto pcol = [&](int g) { return g < skip_at ? g : g + skip_len; };
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < kFM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kFN; ++j) {
       acc[i][j][0] *= sgn;
       acc[i][j][1] *= sgn;
     }
   if (C) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = wm * 64 + i * 8 + fr;
+    for (int i = 0; i < kFM; ++i) {
+      const int r = wm * WTM + i * 8 + fr;
       const int64_t row = m0 + r;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int cl = wn * 32 + j * 8 + 2 * fc;
+      for (int j = 0; j < kFN; ++j) {
+        const int cl = wn * WTN + j * 8 + 2 * fc;
         if (r >= mrem || cl >= nrem) continue;
         const int p0 = pcol(n0 + cl), p1 = pcol(n0 + cl + 1);
         const double* cp = C + row * ldc + p0;
@@ -205,12 +272,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_con
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = wm * 64 + i * 8 + fr;
+  for (int i = 0; i < kFM; ++i) {
+    const int r = wm * WTM + i * 8 + fr;
     const int64_t row = m0 + r;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int cl = wn * 32 + j * 8 + 2 * fc;
+    for (int j = 0; j < kFN; ++j) {
+      const int cl = wn * WTN + j * 8 + 2 * fc;
       if (r >= mrem || cl >= nrem) continue;
       const int p0 = pcol(n0 + cl), p1 = pcol(n0 + cl + 1);
       double* dp = D + row * ldd + p0;
@@ -222,6 +289,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dmma_kernel(const __grid_con
       }
     }
   }
+}
+
+// Variants (selected by BI_GEMM_VARIANT for tuning; default 2: 16 warps of
+// 32x32 -- measured best on every engine and leaf-update shape).
+#define BI_GEMM_VARIANTS(X)                \
+  X(0, 2, 4, 64, 32, 16, 4) /* 8 warps */  \
+  X(1, 2, 4, 64, 32, 32, 3)                \
+  X(2, 4, 4, 32, 32, 16, 4) /* 16 warps */ \
+  X(3, 4, 4, 32, 32, 32, 3)
+
+int g_variant = -1;
+
+int gemm_variant() {
+  if (g_variant < 0) {
+    const char* v = getenv("BI_GEMM_VARIANT");
+    g_variant = v ? atoi(v) : 2;
+    if (g_variant < 0 || g_variant > 3) g_variant = 2;
+  }
+  return g_variant;
 }
 
 std::once_flag g_attr_once;
@@ -243,8 +329,14 @@ int finalize_descs(GemmDesc* d, int count) {
 
 cudaError_t gemm_init_attributes() {
   std::call_once(g_attr_once, [] {
-    g_attr_err = cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSmemBytes);
+    cudaError_t e = cudaSuccess;
+#define BI_SET_ATTR(id, a, b, c, d_, e_, f)                                                       \
+  if (e == cudaSuccess)                                                                       \
+    e = cudaFuncSetAttribute(gemm_dmma_kernel<a, b, c, d_, e_, f>,                            \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<a, b, c, d_, e_, f>::kSmem);
+    BI_GEMM_VARIANTS(BI_SET_ATTR)
+#undef BI_SET_ATTR
+    g_attr_err = e;
   });
   return g_attr_err;
 }
@@ -268,8 +360,17 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
     if (!d_descs) return cudaErrorInvalidValue;
     L.descs = d_descs;
   }
-  gemm_dmma_kernel<<<total, kThreads, kSmemBytes, stream>>>(L);
-  return cudaGetLastError();
+  switch (gemm_variant()) {
+#define BI_LAUNCH(id, a, b, c, d_, e_, f)                                                          \
+  case id:                                                                                     \
+    e = launch_kernel(gemm_dmma_kernel<a, b, c, d_, e_, f>, dim3(total),                        \
+                      dim3(Cfg<a, b, c, d_, e_, f>::kThreads), Cfg<a, b, c, d_, e_, f>::kSmem, stream, 1u, \
+                      L);                                                                      \
+    break;
+    BI_GEMM_VARIANTS(BI_LAUNCH)
+#undef BI_LAUNCH
+  }
+  return e;
 }
 
 }  // namespace bi

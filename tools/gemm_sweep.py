@@ -17,7 +17,9 @@ SHAPES = [  # (m, n, k, batch, accumulate)
     (2048, 2048, 2048, 8, True),
     (4096, 4096, 4096, 1, False),
     (8192, 8192, 8192, 1, False),
-    (512, 480, 32, 32, True),  # K3 trailing update
+    (512, 480, 32, 32, True),  # old K3 trailing update
+    (512, 96, 32, 32, True),   # K3 inner update
+    (512, 384, 128, 32, True),  # K3 outer update
     (256, 256, 256, 64, False),
 ]
 
