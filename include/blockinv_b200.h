@@ -102,6 +102,16 @@ int bi_engine_bind(bi_engine* e,
                    double* minv, int64_t ldi, int64_t stride_i,
                    void* workspace, int64_t workspace_bytes, void* stream);
 int bi_engine_run(bi_engine* e, int first_step, int last_step, int use_graph, void* stream);
+/* End-to-end form with HOST buffers (the drop-in call with NumPy memory):
+ * host_in[z] (ld_in, stride_in) is copied into M per matrix on a copy stream,
+ * M_inv is zeroed (first_step == 1), and each inverse is copied back into
+ * host_out[z] as soon as its lane finishes -- transfers overlap the other
+ * matrices' compute.  Either pointer may be NULL (data already resident / no
+ * read-back).  Page-locked host memory is captured into the step graph;
+ * pageable memory runs the same sequence without a graph. */
+int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t ld_in, int64_t stride_in,
+                       double* host_out, int64_t ld_out, int64_t stride_out,
+                       int first_step, int last_step, int use_graph, void* stream);
 int bi_engine_status(bi_engine* e, int* fail_step, int* fail_quad, int* fail_matrix);
 /* Enqueue only one class of ops of steps [first, last] (no graph): mask 1 =
  * the engine's K1 GEMM launches, 2 = the leaf inversions (K3 incl. their

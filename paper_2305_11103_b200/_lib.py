@@ -37,6 +37,8 @@ SIGNATURES = [
     ("bi_engine_workspace_bytes", _c_i64, [_vp]),
     ("bi_engine_bind", _c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp]),
     ("bi_engine_run", _c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
+    ("bi_engine_run_host", _c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _c_int, _c_int, _c_int,
+                                    _vp]),
     ("bi_engine_status", _c_int, [_vp, _pint, _pint, _pint]),
     ("bi_engine_counters", _c_int, [_vp, _c_int, _c_int, _pdbl]),
     ("bi_engine_run_phase", _c_int, [_vp, _c_int, _c_int, _c_int, _vp]),

@@ -25,6 +25,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/blockinv_b200.h"
@@ -133,6 +134,17 @@ struct Window {
   int64_t ld;
 };
 
+struct GraphKey {
+  int first, last;
+  const void* in;
+  const void* out;
+  int64_t ld_in, s_in, ld_out, s_out;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(first, last, in, out, ld_in, s_in, ld_out, s_out) <
+           std::tie(o.first, o.last, o.in, o.out, o.ld_in, o.s_in, o.ld_out, o.s_out);
+  }
+};
+
 }  // namespace
 
 struct bi_engine {
@@ -173,7 +185,9 @@ struct bi_engine {
   cudaStream_t capture_stream = nullptr;
   cudaStream_t aux_stream[kMaxLanes] = {};  // lanes 1.. (lane 0 runs on the caller's stream)
   cudaEvent_t ev_fork = nullptr, ev_skew[kMaxLanes] = {}, ev_join[kMaxLanes] = {};
-  std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+  cudaStream_t copy_stream = nullptr;       // host->device input copies
+  std::vector<cudaEvent_t> ev_h2d;          // one per matrix
+  std::map<GraphKey, cudaGraphExec_t> graphs;
   int last_first = 1, last_last = 0;
 
   void* meta_dev = nullptr;
@@ -188,6 +202,8 @@ struct bi_engine {
       if (ev_join[l]) cudaEventDestroy(ev_join[l]);
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (cudaEvent_t ev : ev_h2d) cudaEventDestroy(ev);
     if (meta_dev) cudaFree(meta_dev);
   }
 
@@ -447,8 +463,13 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
     const char* pe = getenv("BI_LEAF_PRIORITY");
     e->leaf_priority = (pe && atoi(pe) == 0) ? 0 : high_launch_priority();
   }
-  if (e->nlanes > 1 && !e->ev_fork) {
-    BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+  if (!e->copy_stream) {
+    BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    e->ev_h2d.assign(e->Z, nullptr);
+    for (int z = 0; z < e->Z; ++z) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_h2d[z], cudaEventDisableTiming));
+  }
+  if (!e->ev_fork) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+  if (e->nlanes > 1 && !e->ev_skew[0]) {
     for (int l = 0; l < e->nlanes; ++l) {
       if (l > 0) BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->aux_stream[l], cudaStreamNonBlocking));
       BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_skew[l], cudaEventDisableTiming));
@@ -543,42 +564,96 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
   return cudaSuccess;
 }
 
-static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s, int mask = 3) {
-  if (e->nlanes == 1) return enqueue_lane(e, 0, first, last, s, mask);
+// Optional host I/O around a step range: per-matrix H2D on a copy stream,
+// M_inv zero-fill per lane, per-matrix D2H as soon as its lane finishes.
+struct HostIO {
+  const double* in;
+  int64_t ld_in, s_in;
+  double* out;
+  int64_t ld_out, s_out;
+};
+
+static cudaError_t lane_io_pre(bi_engine* e, int lane, cudaStream_t ls, int first, const HostIO* io) {
+  cudaError_t err = cudaSuccess;
+  for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z) {
+    if (io && io->in) err = cudaStreamWaitEvent(ls, e->ev_h2d[z], 0);
+    if (err == cudaSuccess && io && first == 1)
+      err = cudaMemset2DAsync(e->Minv + (int64_t)z * e->si, e->ldi * 8, 0, e->n * 8, e->n, ls);
+  }
+  return err;
+}
+
+static cudaError_t lane_io_post(bi_engine* e, int lane, cudaStream_t ls, const HostIO* io) {
+  cudaError_t err = cudaSuccess;
+  if (!io || !io->out) return err;
+  for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z)
+    err = cudaMemcpy2DAsync(io->out + (int64_t)z * io->s_out, io->ld_out * 8, e->Minv + (int64_t)z * e->si,
+                            e->ldi * 8, e->n * 8, e->n, cudaMemcpyDeviceToHost, ls);
+  return err;
+}
+
+static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s, int mask = 3,
+                                 const HostIO* io = nullptr) {
+  cudaError_t err = cudaSuccess;
+  const bool fork = e->nlanes > 1 || (io && io->in);
+  if (fork) err = cudaEventRecord(e->ev_fork, s);
+  if (io && io->in && err == cudaSuccess) {
+    err = cudaStreamWaitEvent(e->copy_stream, e->ev_fork, 0);
+    for (int z = 0; z < e->Z && err == cudaSuccess; ++z) {
+      err = cudaMemcpy2DAsync(const_cast<double*>(e->M) + (int64_t)z * e->sm, e->ldm * 8,
+                              io->in + (int64_t)z * io->s_in, io->ld_in * 8, e->n * 8, e->n,
+                              cudaMemcpyHostToDevice, e->copy_stream);
+      if (err == cudaSuccess) err = cudaEventRecord(e->ev_h2d[z], e->copy_stream);
+    }
+  }
   // Lanes: lane l runs on its own stream, starting after lane l-1 completes
   // its first step (a one-step skew per lane); all lanes join back into `s`.
-  cudaError_t err = cudaEventRecord(e->ev_fork, s);
   for (int l = 0; l < e->nlanes && err == cudaSuccess; ++l) {
     cudaStream_t ls = l == 0 ? s : e->aux_stream[l];
     if (l > 0) {
       err = cudaStreamWaitEvent(ls, e->ev_fork, 0);
       if (err == cudaSuccess) err = cudaStreamWaitEvent(ls, e->ev_skew[l - 1], 0);
     }
-    if (err == cudaSuccess) err = enqueue_lane(e, l, first, last, ls, mask, e->ev_skew[l]);
+    if (err == cudaSuccess) err = lane_io_pre(e, l, ls, first, io);
+    if (err == cudaSuccess)
+      err = enqueue_lane(e, l, first, last, ls, mask, e->nlanes > 1 ? e->ev_skew[l] : nullptr);
+  }
+  // read-back after every lane is enqueued (a pageable D2H blocks the host)
+  for (int l = 0; l < e->nlanes && err == cudaSuccess; ++l) {
+    cudaStream_t ls = l == 0 ? s : e->aux_stream[l];
+    err = lane_io_post(e, l, ls, io);
     if (err == cudaSuccess && l > 0) err = cudaEventRecord(e->ev_join[l], ls);
   }
   for (int l = 1; l < e->nlanes && err == cudaSuccess; ++l) err = cudaStreamWaitEvent(s, e->ev_join[l], 0);
   return err;
 }
 
-extern "C" int bi_engine_run(bi_engine* e, int first_step, int last_step, int use_graph, void* stream) {
-  BI_REQUIRE(e && e->bound, "engine not bound");
-  BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step,
-             "stepid outside 1..N_s");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+static bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+static int run_impl(bi_engine* e, int first_step, int last_step, int use_graph, cudaStream_t s, const HostIO* io) {
   e->last_stream = s;
   e->last_first = first_step;
   e->last_last = last_step;
+  if (io && !(is_pinned(io->in) && is_pinned(io->out))) use_graph = 0;  // pageable copies cannot be captured
   if (!use_graph) {
-    BI_CUDA_TRY(enqueue_steps(e, first_step, last_step, s));
+    BI_CUDA_TRY(enqueue_steps(e, first_step, last_step, s, 3, io));
     return 0;
   }
-  auto key = std::make_pair(first_step, last_step);
+  GraphKey key{first_step, last_step, io ? io->in : nullptr, io ? io->out : nullptr,
+               io ? io->ld_in : 0, io ? io->s_in : 0, io ? io->ld_out : 0, io ? io->s_out : 0};
   auto it = e->graphs.find(key);
   if (it == e->graphs.end()) {
     if (!e->capture_stream) BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->capture_stream, cudaStreamNonBlocking));
     BI_CUDA_TRY(cudaStreamBeginCapture(e->capture_stream, cudaStreamCaptureModeThreadLocal));
-    cudaError_t err = enqueue_steps(e, first_step, last_step, e->capture_stream);
+    cudaError_t err = enqueue_steps(e, first_step, last_step, e->capture_stream, 3, io);
     cudaGraph_t graph = nullptr;
     cudaError_t err2 = cudaStreamEndCapture(e->capture_stream, &graph);
     if (err != cudaSuccess || err2 != cudaSuccess) {
@@ -590,10 +665,36 @@ extern "C" int bi_engine_run(bi_engine* e, int first_step, int last_step, int us
     cudaError_t err3 = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     BI_CUDA_TRY(err3);
+    if (e->graphs.size() >= 16) {  // bound the cache
+      cudaGraphExecDestroy(e->graphs.begin()->second);
+      e->graphs.erase(e->graphs.begin());
+    }
     it = e->graphs.emplace(key, exec).first;
   }
   BI_CUDA_TRY(cudaGraphLaunch(it->second, s));
   return 0;
+}
+
+extern "C" int bi_engine_run(bi_engine* e, int first_step, int last_step, int use_graph, void* stream) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step,
+             "stepid outside 1..N_s");
+  return run_impl(e, first_step, last_step, use_graph, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+extern "C" int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t ld_in, int64_t stride_in,
+                                  double* host_out, int64_t ld_out, int64_t stride_out, int first_step,
+                                  int last_step, int use_graph, void* stream) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step,
+             "stepid outside 1..N_s");
+  BI_REQUIRE(!host_in || (ld_in >= e->n && (e->Z == 1 || stride_in >= ld_in * e->n)),
+             "host input leading dimension / stride too small");
+  BI_REQUIRE(!host_out || (ld_out >= e->n && (e->Z == 1 || stride_out >= ld_out * e->n)),
+             "host output leading dimension / stride too small");
+  BI_REQUIRE(!host_in || first_step == 1, "host input requires first_step == 1");
+  HostIO io{host_in, ld_in, stride_in, host_out, ld_out, stride_out};
+  return run_impl(e, first_step, last_step, use_graph, static_cast<cudaStream_t>(stream), &io);
 }
 
 extern "C" int bi_engine_run_phase(bi_engine* e, int first_step, int last_step, int mask, void* stream) {

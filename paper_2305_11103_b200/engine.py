@@ -248,6 +248,34 @@ class DeviceEngine:
         rc = _lib.lib().bi_engine_run(self._h, first, last, 1 if use_graph else 0, _lib.stream_ptr())
         _lib.check(rc, "bi_engine_run")
 
+    def run_host(self, ms: np.ndarray | None, out: np.ndarray | None, first: int = 1, last: int | None = None,
+                 use_graph: bool = True) -> None:
+        """End-to-end on HOST buffers (``bi_engine_run_host``): per-matrix
+        host->device copies of ``ms`` [batch, n, n] overlap the other matrices'
+        compute, and every inverse is copied into ``out`` [batch, n, n] as soon
+        as its lane finishes.  Float64, unit column stride; page-locked buffers
+        are captured into the step graph.  Asynchronous: call ``check()``."""
+        last = self.n_steps if last is None else last
+        n = self.n
+
+        def spec(a, what):
+            if a is None:
+                return None, 0, 0
+            if a.dtype != np.float64 or a.ndim not in (2, 3) or a.strides[-1] != 8:
+                raise DimensionMismatch(f"{what}: float64 array with unit column stride required")
+            a3 = a if a.ndim == 3 else a[None]
+            if a3.shape != (self.batch, n, n):
+                raise DimensionMismatch(f"{what} {a.shape} vs engine ({self.batch}, {n}, {n})")
+            return a3.ctypes.data, a3.strides[1] // 8, a3.strides[0] // 8
+
+        pi, ldi, si = spec(ms, "input")
+        po, ldo, so = spec(out, "output")
+        if po is not None and not out.flags.writeable:
+            raise DimensionMismatch("output array is read-only")
+        rc = _lib.lib().bi_engine_run_host(self._h, pi, ldi, si, po, ldo, so, first, last,
+                                           1 if use_graph else 0, _lib.stream_ptr())
+        _lib.check(rc, "bi_engine_run_host")
+
     def run_phase(self, mask: int, first: int = 1, last: int | None = None) -> None:
         """Enqueue only the K1 GEMM ops (mask 1) or only the leaf inversions
         (mask 2) of steps [first, last] -- per-kernel timing for the roofline."""
@@ -346,15 +374,15 @@ def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backe
     scheme, dense = _scheme_and_dense(m, sizes)
     eng = _engine_for(scheme.sizes, 1)
     last = _last_step(eng.n_steps, stop_after_step)
-    eng.load(dense[None])
-    eng.run(1, last)
+    dense = np.ascontiguousarray(dense, dtype=np.float64)
+    out = np.empty((scheme.m_n, scheme.m_n))
+    eng.run_host(dense, out, 1, last)
     eng.check()
     if counters is not None:
         c = eng.counters(1, last)
         counters.multiplies += c["multiplies"]
         counters.inversions += c["inversions"]
         counters.reductions += c["reductions"]
-    out = eng.Minv[0].cpu().numpy()
     return BlockMatrix(scheme, MemoryBlockStore(scheme, out), role="inverse")
 
 
@@ -364,24 +392,26 @@ def run_inversion_batch(ms, sizes, out: np.ndarray | None = None,
     """Batched extension: invert ``ms`` [batch, n, n] (shared partition
     ``sizes``) in lock-step; returns (or fills ``out``) [batch, n, n].
     Page-locked ``ms``/``out`` make the host<->device copies asynchronous DMA."""
-    t = _lib.torch()
-    ms_t = ms if isinstance(ms, t.Tensor) else t.from_numpy(np.ascontiguousarray(ms, dtype=np.float64))
-    if ms_t.dim() != 3 or ms_t.shape[1] != ms_t.shape[2]:
-        raise DimensionMismatch(f"expected [batch, n, n], got {tuple(ms_t.shape)}")
+    if isinstance(ms, np.ndarray) and ms.dtype == np.float64 and ms.ndim == 3 and ms.strides[-1] == 8:
+        ms_np = ms
+    else:
+        t = _lib.torch()
+        ms_np = ms.cpu().numpy() if isinstance(ms, t.Tensor) else np.ascontiguousarray(ms, dtype=np.float64)
+        ms_np = np.ascontiguousarray(ms_np, dtype=np.float64)
+    if ms_np.ndim != 3 or ms_np.shape[1] != ms_np.shape[2]:
+        raise DimensionMismatch(f"expected [batch, n, n], got {ms_np.shape}")
     scheme = partition_from_sizes(sizes)
-    if scheme.m_n != ms_t.shape[1]:
-        raise DimensionMismatch(f"sizes sum to {scheme.m_n}, matrix order is {ms_t.shape[1]}")
-    eng = _engine_for(scheme.sizes, int(ms_t.shape[0]))
+    if scheme.m_n != ms_np.shape[1]:
+        raise DimensionMismatch(f"sizes sum to {scheme.m_n}, matrix order is {ms_np.shape[1]}")
+    eng = _engine_for(scheme.sizes, int(ms_np.shape[0]))
     last = _last_step(eng.n_steps, stop_after_step)
-    eng.load(ms_t, non_blocking=True)
-    eng.run(1, last)
+    if out is None:
+        out = np.empty(ms_np.shape)
+    eng.run_host(ms_np, out, 1, last)
     eng.check()
     if counters is not None:
         c = eng.counters(1, last)
         counters.multiplies += c["multiplies"]
         counters.inversions += c["inversions"]
         counters.reductions += c["reductions"]
-    if out is None:
-        out = np.empty(tuple(ms_t.shape))
-    t.from_numpy(out).copy_(eng.Minv)
     return out
