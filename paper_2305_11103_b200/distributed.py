@@ -1,0 +1,357 @@
+"""Multi-GPU level scheduler for the step engine: one process per
+GPU, torch.distributed (NCCL over NVLink) for the exchanges.
+
+Partitioning (engine.py:313-437): with P ranks
+and N_b diagonal blocks (P | N_b), rank r owns the home range of blocks
+H_r = [r N_b/P, (r+1) N_b/P) and stores *block columns* H_r of M, M_inv and of
+every provisional set T_l (all rows).  The step schedule is the reference's
+(stepid -> loopid -> action, engine.py:73-162), executed by every rank:
+
+* diag (leaf inversions)  -- every leaf block lies in one home range: local;
+* arrows at a local level -- the quad lies in one home range: local;
+* arrows at a global level (the quad spans a rank group G = G_A u G_D): each
+  rank sends its (side x w) column slab -- G_A ranks [A^-1 ; C], G_D ranks
+  [B ; D^-1] -- in one all-gather inside G; G_A ranks then form their columns
+  of L = -D^-1 C and S_D = A + B L, G_D ranks their columns of R = -A^-1 B and
+  S_A = D + C R;
+* up/down pass at a global level -- G_A ranks all-gather L, G_D ranks R,
+  then each forms its columns of M_inv[D, A] = L M_inv[A, A] /
+  M_inv[A, D] = R M_inv[D, D].
+
+Every GEMM is split by output columns only (K is never split), so the
+inverse is bitwise identical for every P (the GPU analogue of the reference's
+worker-count determinism, test_acceptance.py:146-156).
+
+The compute backend defaults to the B200 kernels (K1 GEMM, K3 leaf
+inversion through the C ABI).  ``backend=`` accepts any object with the same
+three methods; the CPU multi-process tests use that to exercise this
+schedule and its collectives with the gloo backend.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .engine import decode_step, loopid_for_step, total_steps, INVERT_DIAGONALS, ARROWS_AND_SCHUR
+from .errors import DimensionMismatch, InvalidOrder, SingularBlock
+from .partition import partition_from_sizes
+
+
+class DeviceBackend:
+    """B200 kernels through the C ABI (K1 / K3)."""
+
+    def __init__(self):
+        from . import _lib
+
+        self._lib = _lib
+        self.device = _lib.require_device()
+
+    def empty(self, rows: int, cols: int):
+        return self._lib.empty_matrix(rows, cols)
+
+    def gemm(self, a, b, d, c=None, negate=False):
+        from .core import device_gemm
+
+        device_gemm(a, b, d, c=c, negate=negate)
+
+    def inverse(self, blocks, outs):
+        """blocks/outs: [count, b, b] strided views; returns info (numpy)."""
+        from .core import device_inverse
+
+        return device_inverse(blocks, outs)
+
+
+def _group_ranks(rank: int, group_size: int) -> list[int]:
+    g0 = rank // group_size * group_size
+    return list(range(g0, g0 + group_size))
+
+
+class ShardedEngine:
+    """One rank's share of the step engine for ``sizes`` over a process group."""
+
+    def __init__(self, sizes, group=None, backend=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group if group is not None else dist.group.WORLD
+        self.P = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.scheme = partition_from_sizes(sizes)
+        self.sizes = list(self.scheme.sizes)
+        self.nb = len(self.sizes)
+        if self.P & (self.P - 1) or self.nb % self.P:
+            raise InvalidOrder(f"{self.P} ranks must be a power of two dividing {self.nb} blocks")
+        self.off = list(self.scheme.offsets)
+        self.n = self.scheme.m_n
+        self.k = self.nb.bit_length() - 1
+        self.nbp = self.nb // self.P  # blocks per rank
+        self.h0 = self.rank * self.nbp
+        self.h1 = self.h0 + self.nbp
+        self.c0 = self.off[self.h0]
+        self.w = self.off[self.h1] - self.c0
+        self.be = backend if backend is not None else DeviceBackend()
+        # column-slab storage
+        self.M = self.be.empty(self.n, self.w)
+        self.Minv = self.be.empty(self.n, self.w)
+        self.T = {}
+        for lv in range(1, self.k + 1):
+            for g in range(self.nb >> lv):
+                first, last = g << lv, (g + 1) << lv
+                if last <= self.h0 or first >= self.h1:
+                    continue
+                side = self.off[last] - self.off[first]
+                cols = self.off[min(last, self.h1)] - self.off[max(first, self.h0)]
+                self.T[(lv, g)] = self.be.empty(side, cols)
+        # rank groups for the global levels (created collectively, same order everywhere)
+        self.groups = {}
+        world_ranks = list(range(self.P))
+        gs = 2
+        while gs <= self.P:
+            for g0 in range(0, self.P, gs):
+                members = world_ranks[g0:g0 + gs]
+                pg = dist.new_group([dist.get_global_rank(self.group, m) for m in members]) \
+                    if self.group is not dist.group.WORLD else dist.new_group(members)
+                if self.rank in members:
+                    self.groups[gs] = pg
+            gs *= 2
+
+    # -- layout helpers -----------------------------------------------------
+    def is_global(self, level: int) -> bool:
+        return (1 << level) > self.nbp
+
+    def _cols(self, c0: int, c1: int) -> tuple[int, int]:
+        if c0 < self.h0 or c1 > self.h1:
+            raise IndexError(f"block columns {c0}:{c1} not on rank {self.rank}")
+        return self.off[c0] - self.c0, self.off[c1] - self.c0
+
+    def m_win(self, r0, r1, c0, c1):
+        a, b = self._cols(c0, c1)
+        return self.M[self.off[r0]:self.off[r1], a:b]
+
+    def minv_win(self, r0, r1, c0, c1):
+        a, b = self._cols(c0, c1)
+        return self.Minv[self.off[r0]:self.off[r1], a:b]
+
+    def t_win(self, level, r0, r1, c0, c1):
+        g = min(r0, c0) >> level
+        sq = self.T[(level, g)]
+        o = self.off[g << level]
+        col_origin = max(self.off[g << level], self.c0)
+        a = self.off[c0] - col_origin
+        b = self.off[c1] - col_origin
+        return sq[self.off[r0] - o:self.off[r1] - o, a:b]
+
+    def src_win(self, act, r0, r1, c0, c1):
+        if act.source == "matrix":
+            return self.m_win(r0, r1, c0, c1)
+        return self.t_win(act.cid, r0, r1, c0, c1)
+
+    # -- step actions -------------------------------------------------------
+    def _diag(self, act, stepid):
+        blocks = list(range(self.h0, self.h1))
+        # group runs of equal-size consecutive blocks inside one buffer
+        runs, cur = [], [blocks[0]]
+        for p in blocks[1:]:
+            same_buf = act.source == "matrix" or (p >> act.cid) == (cur[0] >> act.cid)
+            if self.sizes[p] == self.sizes[cur[0]] and same_buf:
+                cur.append(p)
+            else:
+                runs.append(cur)
+                cur = [p]
+        runs.append(cur)
+        for run in runs:
+            b = self.sizes[run[0]]
+            src0 = self.src_win(act, run[0], run[0] + 1, run[0], run[0] + 1)
+            dst0 = self.minv_win(run[0], run[0] + 1, run[0], run[0] + 1)
+            cnt = len(run)
+            src = src0.as_strided((cnt, b, b), (b * (src0.stride(0) + 1), src0.stride(0), 1))
+            dst = dst0.as_strided((cnt, b, b), (b * (dst0.stride(0) + 1), dst0.stride(0), 1))
+            info = self.be.inverse(src, dst)
+            bad = np.nonzero(np.asarray(info))[0]
+            if len(bad) and self._first_fail is None:
+                self._first_fail = (stepid, run[int(bad[0])])
+
+    def _quad(self, level, g):
+        first = g << level
+        mid = first + (1 << (level - 1))
+        return first, mid, (g + 1) << level
+
+    def _allgather_tensor(self, send, pg, size):
+        """[size, *send.shape] all-gather: NCCL device-to-device; gloo (CPU
+        tests, or several ranks sharing one GPU) stages through host memory."""
+        import torch
+
+        send = send.contiguous()
+        if self.dist.get_backend(pg) == "nccl":
+            recv = torch.empty((size,) + tuple(send.shape), dtype=send.dtype, device=send.device)
+            self.dist.all_gather_into_tensor(recv, send, group=pg)
+            return recv
+        host = send.cpu()
+        parts = [torch.empty_like(host) for _ in range(size)]
+        self.dist.all_gather(parts, host, group=pg)
+        return torch.stack(parts).to(send.device)
+
+    def _width(self, r: int) -> int:
+        return self.off[(r + 1) * self.nbp] - self.off[r * self.nbp]
+
+    def _allgather(self, level, slab):
+        """All-gather column slabs inside this rank's level-`level` group; slabs
+        are padded to the group's widest home range and trimmed on receipt."""
+        import torch
+
+        gs = (1 << level) // self.nbp
+        members = _group_ranks(self.rank, gs)
+        wmax = max(self._width(m) for m in members)
+        if slab.shape[1] < wmax:
+            padded = torch.zeros((slab.shape[0], wmax), dtype=slab.dtype, device=slab.device)
+            padded[:, :slab.shape[1]] = slab
+            slab = padded
+        recv = self._allgather_tensor(slab, self.groups[gs], gs)
+        return [recv[i][:, :self._width(m)] for i, m in enumerate(members)], members
+
+    def _arrows(self, act):
+        lv = act.sid
+        be = self.be
+        if not self.is_global(lv):
+            for g in range(self.h0 >> lv, self.h1 >> lv):
+                first, mid, last = self._quad(lv, g)
+                A = self.src_win(act, first, mid, first, mid)
+                B = self.src_win(act, first, mid, mid, last)
+                C = self.src_win(act, mid, last, first, mid)
+                D = self.src_win(act, mid, last, mid, last)
+                R = self.t_win(lv, first, mid, mid, last)
+                L = self.t_win(lv, mid, last, first, mid)
+                be.gemm(self.minv_win(first, mid, first, mid), B, R, negate=True)
+                be.gemm(self.minv_win(mid, last, mid, last), C, L, negate=True)
+                be.gemm(B, L, self.t_win(lv, first, mid, first, mid), c=A)
+                be.gemm(C, R, self.t_win(lv, mid, last, mid, last), c=D)
+            return
+        import torch
+
+        g = self.h0 >> lv
+        first, mid, last = self._quad(lv, g)
+        in_a = self.h1 <= mid
+        ha = self.off[mid] - self.off[first]
+        # my slab: A-half ranks send [A^-1 ; C] cols, D-half ranks [B ; D^-1] cols
+        mine = (self.h0, self.h1)
+        if in_a:
+            top = self.minv_win(first, mid, *mine)
+            bot = self.src_win(act, mid, last, *mine)
+        else:
+            top = self.src_win(act, first, mid, *mine)
+            bot = self.minv_win(mid, last, *mine)
+        slab = torch.cat([top, bot], dim=0)
+        recv, members = self._allgather(lv, slab)
+        peers = [i for i, m in enumerate(members) if (self._rank_h1(m) <= mid) != in_a]
+        top_full = torch.cat([recv[i][:ha] for i in peers], dim=1)   # A^-1 or B
+        bot_full = torch.cat([recv[i][ha:] for i in peers], dim=1)   # C or D^-1
+        if in_a:
+            B, Dinv = top_full, bot_full
+            C_my = self.src_win(act, mid, last, *mine)
+            A_my = self.src_win(act, first, mid, *mine)
+            L_my = self.t_win(lv, mid, last, *mine)
+            self.be.gemm(Dinv, C_my, L_my, negate=True)
+            self.be.gemm(B, L_my, self.t_win(lv, first, mid, *mine), c=A_my)
+        else:
+            Ainv, C = top_full, bot_full
+            B_my = self.src_win(act, first, mid, *mine)
+            D_my = self.src_win(act, mid, last, *mine)
+            R_my = self.t_win(lv, first, mid, *mine)
+            self.be.gemm(Ainv, B_my, R_my, negate=True)
+            self.be.gemm(C, R_my, self.t_win(lv, mid, last, *mine), c=D_my)
+
+    def _rank_h1(self, r):
+        return (r + 1) * self.nbp
+
+    def _updown(self, lv):
+        be = self.be
+        if not self.is_global(lv):
+            for g in range(self.h0 >> lv, self.h1 >> lv):
+                first, mid, last = self._quad(lv, g)
+                be.gemm(self.t_win(lv, mid, last, first, mid), self.minv_win(first, mid, first, mid),
+                        self.minv_win(mid, last, first, mid))
+                be.gemm(self.t_win(lv, first, mid, mid, last), self.minv_win(mid, last, mid, last),
+                        self.minv_win(first, mid, mid, last))
+            return
+        import torch
+
+        g = self.h0 >> lv
+        first, mid, last = self._quad(lv, g)
+        in_a = self.h1 <= mid
+        mine = (self.h0, self.h1)
+        ha, hd = self.off[mid] - self.off[first], self.off[last] - self.off[mid]
+        hmax = max(ha, hd)
+        # A-half ranks carry their L columns (C position), D-half ranks their R columns
+        part = self.t_win(lv, mid, last, *mine) if in_a else self.t_win(lv, first, mid, *mine)
+        slab = torch.zeros((hmax, part.shape[1]), dtype=part.dtype, device=part.device)
+        slab[:part.shape[0]] = part
+        recv, members = self._allgather(lv, slab)
+        same = [i for i, m in enumerate(members) if (self._rank_h1(m) <= mid) == in_a]
+        if in_a:
+            L = torch.cat([recv[i][:hd] for i in same], dim=1)        # hd x ha
+            be.gemm(L, self.minv_win(first, mid, *mine), self.minv_win(mid, last, *mine))
+        else:
+            R = torch.cat([recv[i][:ha] for i in same], dim=1)        # ha x hd
+            be.gemm(R, self.minv_win(mid, last, *mine), self.minv_win(first, mid, *mine))
+
+    # -- driver -------------------------------------------------------------
+    def load(self, m: np.ndarray) -> None:
+        """Copy this rank's column slab of the full matrix ``m``."""
+        import torch
+
+        if m.shape != (self.n, self.n):
+            raise DimensionMismatch(f"matrix {m.shape} vs order {self.n}")
+        self.M.copy_(torch.from_numpy(np.ascontiguousarray(m[:, self.c0:self.c0 + self.w])))
+
+    def run(self, first: int = 1, last: int | None = None) -> None:
+        nsteps = total_steps(self.nb)
+        last = nsteps if last is None else last
+        if first == 1:
+            self.Minv.zero_()
+        self._first_fail = None
+        for stepid in range(first, last + 1):
+            act = decode_step(loopid_for_step(stepid, self.nb))
+            if act.kind == INVERT_DIAGONALS:
+                self._diag(act, stepid)
+            elif act.kind == ARROWS_AND_SCHUR:
+                self._arrows(act)
+            else:
+                self._diag(act, stepid)
+                for lv in range(1, act.depth + 1):
+                    self._updown(lv)
+
+    def check(self) -> None:
+        """Raise SingularBlock(step, quad) for the first singular leaf on any
+        rank (engine.py:320-328); collective."""
+        import torch
+
+        mine = self._first_fail or (1 << 30, 1 << 30)
+        t = torch.tensor([mine[0] * (self.nb + 1) + mine[1]], dtype=torch.int64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.to(self.M.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        v = int(t.item())
+        if v < (1 << 30) * (self.nb + 1):
+            raise SingularBlock("A", path=[], step=v // (self.nb + 1), quad=v % (self.nb + 1))
+
+    def gather(self) -> np.ndarray:
+        """The full inverse (collective; every rank receives it)."""
+        import torch
+
+        wmax = max(self._width(r) for r in range(self.P))
+        send = torch.zeros((self.n, wmax), dtype=self.Minv.dtype, device=self.Minv.device)
+        send[:, :self.w] = self.Minv
+        recv = self._allgather_tensor(send, self.group, self.P)
+        return torch.cat([recv[r][:, :self._width(r)] for r in range(self.P)], dim=1).cpu().numpy()
+
+
+def run_inversion_sharded(m, sizes, group=None, backend=None, stop_after_step=None) -> np.ndarray:
+    """run_inversion (engine.py:482-542) with the matrix column-sharded over the
+    ranks of ``group`` (one process per GPU).  Every rank passes the same
+    ``m``; every rank receives the full inverse.  Raises SingularBlock like the
+    single-device engine."""
+    eng = ShardedEngine(sizes, group=group, backend=backend)
+    eng.load(np.asarray(m, dtype=np.float64))
+    eng.run(1, stop_after_step)
+    eng.check()
+    return eng.gather()

@@ -1,0 +1,112 @@
+"""Multi-process tests of the column-sharded level scheduler.
+
+CPU (gloo, world sizes 2 and 4): the schedule, ownership and collectives of
+paper_2305_11103_b200.distributed run with a torch-CPU compute backend defined
+here (test infrastructure), checked against the oracle engine.
+GPU: two processes share the one B200 (gloo collectives, B200 kernels) and
+must reproduce the single-device engine bit for bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from conftest import well_conditioned
+
+
+class TorchCPUBackend:
+    """float64 torch-CPU primitives with the oracle's pivoted GJ leaf."""
+
+    def empty(self, rows, cols):
+        return torch.empty((rows, cols), dtype=torch.float64)
+
+    def gemm(self, a, b, d, c=None, negate=False):
+        prod = a @ b
+        res = (c.clone() if c is not None else torch.zeros_like(d)) + (-prod if negate else prod)
+        d.copy_(res)
+
+    def inverse(self, blocks, outs):
+        info = np.zeros(blocks.shape[0], dtype=np.int32)
+        for i in range(blocks.shape[0]):
+            try:
+                outs[i].copy_(torch.from_numpy(oracle.gauss_jordan(blocks[i].numpy())))
+            except oracle.OracleSingularMatrix:
+                info[i] = 1
+        return info
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, sizes, seed, device, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_11103_b200.distributed import run_inversion_sharded
+
+        n = sum(sizes)
+        m = well_conditioned(n, seed)
+        backend = TorchCPUBackend() if not device else None
+        if device:
+            torch.cuda.set_device(0)
+        inv = run_inversion_sharded(m, sizes, backend=backend)
+        q.put((rank, inv))
+    except Exception as exc:  # surface worker failures in the parent
+        q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, sizes, seed, device=False):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, sizes, seed, device, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, v = q.get(timeout=600)
+        out[r] = v
+    for p in procs:
+        p.join(timeout=60)
+    for r, v in out.items():
+        assert not isinstance(v, str), f"rank {r}: {v}"
+    return out
+
+
+@pytest.mark.parametrize("world,sizes", [(2, [6] * 4), (2, [5, 7, 6, 4, 8, 3, 5, 6]), (2, [3, 9, 2, 4]),
+                                         (4, [8] * 8), (4, [2, 7, 5, 3, 6, 4, 9, 1])])
+def test_sharded_schedule_cpu_gloo(world, sizes):
+    n = sum(sizes)
+    seed = 900 + n
+    out = _run(world, sizes, seed)
+    ref = oracle.run_inversion(well_conditioned(n, seed), sizes=sizes, leaf_inverter=oracle.gauss_jordan)
+    for r in range(world):
+        assert np.max(np.abs(out[r] - ref)) <= 1e-12 * n
+    assert all(np.array_equal(out[0], out[r]) for r in range(world))
+
+
+@pytest.mark.gpu
+def test_sharded_two_ranks_one_gpu_bitwise():
+    import paper_2305_11103_b200 as bi
+
+    sizes = [64] * 8
+    n = sum(sizes)
+    seed = 77
+    out = _run(2, sizes, seed, device=True)
+    single = bi.run_inversion(well_conditioned(n, seed), sizes=sizes).to_dense()
+    assert np.array_equal(out[0], single)
+    assert np.array_equal(out[1], single)
