@@ -133,9 +133,13 @@ int bi_engine_destroy(bi_engine* e);
  * pivot = 'A' : invert_via_a (schur.py:114-139, Eq. 2)
  * pivot = 'D' : invert_via_d (schur.py:142-164, Eq. 3; the singular-A11 path)
  * pivot = 'X' : invert_via_ad (schur.py:219-259, Eq. 7)
+ * counter-diagonal layout (rows split at p, columns at n - p; schur.py:92-101):
+ * pivot = 'B' : invert_via_b (schur.py:167-190)
+ * pivot = 'C' : invert_via_c (schur.py:193-216)
+ * pivot = 'Y' : invert_via_bc (schur.py:262-297)
  * Sub-inversions use K3.  On a singular pivot returns BI_ESINGULAR with
- * *fail_block = 'A','D','a' (SchurA) or 'd' (SchurD) -- the labels of
- * schur._sub_inverse (schur.py:104-111).  out (n x n) must not alias m.
+ * *fail_block = 'A','D','B','C' or 'a','d','b','c' (SchurA/D/B/C) -- the
+ * labels of schur._sub_inverse (schur.py:104-111).  out must not alias m.
  * ---------------------------------------------------------------------- */
 int64_t bi_schur2x2_workspace_bytes(int64_t n, int64_t p);
 int bi_schur2x2(int pivot, int64_t n, int64_t p,

@@ -37,6 +37,9 @@ __all__ = [
     "invert_via_a",
     "invert_via_d",
     "invert_via_ad",
+    "invert_via_b",
+    "invert_via_c",
+    "invert_via_bc",
     "invert_with_fallback",
     "small_sub",
     "by_a_sub",
@@ -576,12 +579,79 @@ def invert_via_ad(m: np.ndarray, split: int, invert_sub, out: np.ndarray) -> Non
     multiply(n_dc, out[:p, :p], out[p:, :p])
 
 
+def _cquad(m, split):
+    """schur.py:92-101: rows split at `split`, columns at n - split."""
+    cs = m.shape[0] - split
+    return m[:split, :cs], m[:split, cs:], m[split:, :cs], m[split:, cs:]
+
+
+def invert_via_b(m: np.ndarray, split: int, invert_sub, out: np.ndarray) -> None:
+    """schur.py:167-190: square off-diagonal pivot B, S_B = C - D B^-1 A."""
+    a, b, c, d = _cquad(m, split)
+    p, w = b.shape[0], c.shape[0]
+    binv = _sub(invert_sub, b, "B")
+    n_ba = np.empty_like(a)
+    multiply(binv, a, n_ba, negate=True)
+    db = np.empty_like(d)
+    multiply(d, binv, db)
+    s_b = c.copy()
+    multiply(d, n_ba, s_b, accumulate=True)
+    sinv = _sub(invert_sub, s_b, "SchurB")
+    multiply(n_ba, sinv, out[w:, p:])
+    out[w:, :p] = binv
+    multiply(out[w:, p:], db, out[w:, :p], accumulate=True, negate=True)
+    multiply(sinv, db, out[:w, :p], negate=True)
+    out[:w, p:] = sinv
+
+
+def invert_via_c(m: np.ndarray, split: int, invert_sub, out: np.ndarray) -> None:
+    """schur.py:193-216: square off-diagonal pivot C, S_C = B - A C^-1 D."""
+    a, b, c, d = _cquad(m, split)
+    p, w = b.shape[0], c.shape[0]
+    cinv = _sub(invert_sub, c, "C")
+    n_cd = np.empty_like(d)
+    multiply(cinv, d, n_cd, negate=True)
+    ac = np.empty_like(a)
+    multiply(a, cinv, ac)
+    s_c = b.copy()
+    multiply(a, n_cd, s_c, accumulate=True)
+    sinv = _sub(invert_sub, s_c, "SchurC")
+    multiply(n_cd, sinv, out[:w, :p])
+    out[:w, p:] = cinv
+    multiply(out[:w, :p], ac, out[:w, p:], accumulate=True, negate=True)
+    multiply(sinv, ac, out[w:, p:], negate=True)
+    out[w:, :p] = sinv
+
+
+def invert_via_bc(m: np.ndarray, split: int, invert_sub, out: np.ndarray) -> None:
+    """schur.py:262-297: both counter-diagonal pivots."""
+    a, b, c, d = _cquad(m, split)
+    p, w = b.shape[0], c.shape[0]
+    binv = _sub(invert_sub, b, "B")
+    cinv = _sub(invert_sub, c, "C")
+    n_ba = np.empty_like(a)
+    multiply(binv, a, n_ba, negate=True)
+    n_cd = np.empty_like(d)
+    multiply(cinv, d, n_cd, negate=True)
+    s_b = c.copy()
+    mm_acc(d, n_ba, s_b)
+    s_c = b.copy()
+    mm_acc(a, n_cd, s_c)
+    for blk, view, label in ((s_b, out[:w, p:], "SchurB"), (s_c, out[w:, :p], "SchurC")):
+        try:
+            invert_sub(blk, view)
+        except OracleSingular as exc:
+            raise OracleSingular(label, exc.path) from None
+    multiply(n_cd, out[w:, :p], out[:w, :p])
+    multiply(n_ba, out[:w, p:], out[w:, p:])
+
+
 def invert_with_fallback(m: np.ndarray, split: int, out: np.ndarray, invert_sub=None) -> str:
-    """schur.py:300-333, diagonal pivots only (A then D); the counter-diagonal
-    B/C formulas are outside the restated hot path (SURVEY 8f #2)."""
+    """schur.py:300-333: pivots in the fixed order A, D, B, C."""
     invert_sub = invert_sub or small_sub
     errs = []
-    for name, fn in (("via_a", invert_via_a), ("via_d", invert_via_d)):
+    for name, fn in (("via_a", invert_via_a), ("via_d", invert_via_d), ("via_b", invert_via_b),
+                     ("via_c", invert_via_c)):
         try:
             fn(m, split, invert_sub, out)
             return name

@@ -213,7 +213,8 @@ extern "C" int64_t bi_schur2x2_workspace_bytes(int64_t n, int64_t p) {
 
 extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int64_t ldm, double* out,
                            int64_t ldo, void* workspace, int64_t workspace_bytes, int* fail_block, void* stream) {
-  BI_REQUIRE(pivot == 'A' || pivot == 'D' || pivot == 'X', "pivot must be 'A', 'D' or 'X'");
+  BI_REQUIRE(pivot == 'A' || pivot == 'D' || pivot == 'X' || pivot == 'B' || pivot == 'C' || pivot == 'Y',
+             "pivot must be 'A', 'D', 'X', 'B', 'C' or 'Y'");
   BI_REQUIRE(p >= 1 && p < n, "split outside 1..n-1");
   BI_REQUIRE(m && out && workspace, "null argument");
   BI_REQUIRE(ldm >= n && ldo >= n, "leading dimension too small");
@@ -245,10 +246,63 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
   double* o01 = out + p;
   double* o10 = out + p * ldo;
   double* o11 = out + p * ldo + p;
-  // info slots: 0 = A, 1 = D, 2 = SchurA, 3 = SchurD
-  char labels[4] = {'A', 'D', 'a', 'd'};
+  // info slots: 0 = A, 1 = D, 2 = SchurA, 3 = SchurD, 4 = B, 5 = C, 6 = SchurB, 7 = SchurC
+  char labels[8] = {'A', 'D', 'a', 'd', 'B', 'C', 'b', 'c'};
   int order[4] = {0, 1, 2, 3};
-  if (pivot == 'A') {
+  // counter-diagonal layout (schur.py:92-101): rows split at p, columns at q = n - p
+  const double* cA = m;                 // p x q
+  const double* cB = m + q;             // p x p
+  const double* cC = m + p * ldm;       // q x q
+  const double* cD = m + p * ldm + q;   // q x p
+  double* oTL = out;                    // q x p
+  double* oTR = out + p;                // q x q
+  double* oBL = out + q * ldo;          // p x p
+  double* oBR = out + q * ldo + p;      // p x q
+  if (pivot == 'B') {
+    // schur.py:167-190, S_B = C - D B^-1 A
+    BI_CUDA_TRY(inv1(p, cB, ldm, Pinv, p, scratch, info + 4, s));
+    BI_CUDA_TRY(gemm1(p, q, p, 1, Pinv, p, cA, ldm, nullptr, 0, Y, q, s));     // Y = -B^-1 A
+    BI_CUDA_TRY(gemm1(q, p, p, 0, cD, ldm, Pinv, p, nullptr, 0, X, p, s));     // X = D B^-1
+    BI_CUDA_TRY(gemm1(q, q, p, 0, cD, ldm, Y, q, cC, ldm, S, q, s));           // S_B = C + D Y
+    BI_CUDA_TRY(inv1(q, S, q, oTR, ldo, scratch, info + 6, s));                // out[:q, p:] = S_B^-1
+    BI_CUDA_TRY(gemm1(p, q, q, 0, Y, q, oTR, ldo, nullptr, 0, oBR, ldo, s));   // out[q:, p:] = Y S_B^-1
+    BI_CUDA_TRY(gemm1(p, p, q, 1, oBR, ldo, X, p, Pinv, p, oBL, ldo, s));      // out[q:, :p] = B^-1 - . X
+    BI_CUDA_TRY(gemm1(q, p, q, 1, oTR, ldo, X, p, nullptr, 0, oTL, ldo, s));   // out[:q, :p] = -S_B^-1 X
+    order[0] = 4;
+    order[1] = 6;
+    order[2] = 4;
+    order[3] = 6;
+  } else if (pivot == 'C') {
+    // schur.py:193-216, S_C = B - A C^-1 D
+    BI_CUDA_TRY(inv1(q, cC, ldm, Qinv, q, scratch, info + 5, s));
+    BI_CUDA_TRY(gemm1(q, p, q, 1, Qinv, q, cD, ldm, nullptr, 0, X, p, s));     // X = -C^-1 D
+    BI_CUDA_TRY(gemm1(p, q, q, 0, cA, ldm, Qinv, q, nullptr, 0, Y, q, s));     // Y = A C^-1
+    BI_CUDA_TRY(gemm1(p, p, q, 0, cA, ldm, X, p, cB, ldm, S, p, s));           // S_C = B + A X
+    BI_CUDA_TRY(inv1(p, S, p, oBL, ldo, scratch, info + 7, s));                // out[q:, :p] = S_C^-1
+    BI_CUDA_TRY(gemm1(q, p, p, 0, X, p, oBL, ldo, nullptr, 0, oTL, ldo, s));   // out[:q, :p] = X S_C^-1
+    BI_CUDA_TRY(gemm1(q, q, p, 1, oTL, ldo, Y, q, Qinv, q, oTR, ldo, s));      // out[:q, p:] = C^-1 - . Y
+    BI_CUDA_TRY(gemm1(p, q, p, 1, oBL, ldo, Y, q, nullptr, 0, oBR, ldo, s));   // out[q:, p:] = -S_C^-1 Y
+    order[0] = 5;
+    order[1] = 7;
+    order[2] = 5;
+    order[3] = 7;
+  } else if (pivot == 'Y') {
+    // schur.py:262-297 (combined counter-diagonal form)
+    BI_CUDA_TRY(inv1(p, cB, ldm, Pinv, p, scratch, info + 4, s));
+    BI_CUDA_TRY(inv1(q, cC, ldm, Qinv, q, scratch, info + 5, s));
+    BI_CUDA_TRY(gemm1(p, q, p, 1, Pinv, p, cA, ldm, nullptr, 0, Y, q, s));     // Y = -B^-1 A
+    BI_CUDA_TRY(gemm1(q, p, q, 1, Qinv, q, cD, ldm, nullptr, 0, X, p, s));     // X = -C^-1 D
+    BI_CUDA_TRY(gemm1(q, q, p, 0, cD, ldm, Y, q, cC, ldm, S, q, s));           // S_B = C + D Y
+    BI_CUDA_TRY(inv1(q, S, q, oTR, ldo, scratch, info + 6, s));                // out[:q, p:] = S_B^-1
+    BI_CUDA_TRY(gemm1(p, p, q, 0, cA, ldm, X, p, cB, ldm, S, p, s));           // S_C = B + A X
+    BI_CUDA_TRY(inv1(p, S, p, oBL, ldo, scratch, info + 7, s));                // out[q:, :p] = S_C^-1
+    BI_CUDA_TRY(gemm1(q, p, p, 0, X, p, oBL, ldo, nullptr, 0, oTL, ldo, s));   // out[:q, :p] = X S_C^-1
+    BI_CUDA_TRY(gemm1(p, q, q, 0, Y, q, oTR, ldo, nullptr, 0, oBR, ldo, s));   // out[q:, p:] = Y S_B^-1
+    order[0] = 4;
+    order[1] = 5;
+    order[2] = 6;
+    order[3] = 7;
+  } else if (pivot == 'A') {
     // schur.py:114-139
     BI_CUDA_TRY(inv1(p, A, ldm, Pinv, p, scratch, info + 0, s));
     BI_CUDA_TRY(gemm1(p, q, p, 1, Pinv, p, B, ldm, nullptr, 0, Y, q, s));      // Y = -A^-1 B

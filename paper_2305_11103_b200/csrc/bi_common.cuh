@@ -123,6 +123,14 @@ cudaError_t launch_residual(int64_t n, int batch, const double* a, int64_t lda, 
 // the latency-bound leaf inversions so their CTAs win freed SMs from the
 // throughput-bound GEMMs of the other lane.
 extern thread_local int g_launch_priority;
+// Upper bound on K1 grid size (0 = one CTA per tile); K1 is persistent over
+// tiles, so a capped launch still covers every tile.
+extern thread_local int g_gemm_grid_cap;
+struct GemmCapScope {
+  int saved;
+  explicit GemmCapScope(int c) : saved(g_gemm_grid_cap) { g_gemm_grid_cap = c; }
+  ~GemmCapScope() { g_gemm_grid_cap = saved; }
+};
 struct PriorityScope {
   int saved;
   explicit PriorityScope(int p) : saved(g_launch_priority) { g_launch_priority = p; }

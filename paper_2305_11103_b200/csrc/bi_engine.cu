@@ -170,6 +170,7 @@ struct bi_engine {
   void* inv_base[kMaxLanes] = {};
   int nlanes = 1;
   int leaf_priority = 0;
+  int gemm_cap = 0;  // engine GEMM grid cap (SMs left for the leaf chains)
   int zlo[kMaxLanes] = {}, zhi[kMaxLanes] = {};
   int* info = nullptr;
   GemmDesc* d_descs = nullptr;
@@ -462,6 +463,12 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   {
     const char* pe = getenv("BI_LEAF_PRIORITY");
     e->leaf_priority = (pe && atoi(pe) == 0) ? 0 : high_launch_priority();
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const char* rs = getenv("BI_RESERVE_SMS");
+    const int reserve = rs ? atoi(rs) : (e->nlanes > 1 ? 16 : 0);
+    e->gemm_cap = (reserve > 0 && reserve < nsm) ? nsm - reserve : 0;
   }
   if (!e->copy_stream) {
     BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
@@ -551,6 +558,7 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
         PriorityScope ps(e->leaf_priority);
         err = launch_inv_group(e->invs[op.index].g, s);
       } else {
+        GemmCapScope cap(e->gemm_cap);
         const GemmLaunchRec& L = e->launches[op.index];
         err = launch_gemm(e->descs.data() + L.first, e->d_descs + L.first, L.count, s);
       }

@@ -23,6 +23,7 @@
 namespace bi {
 
 thread_local int g_launch_priority = 0;
+thread_local int g_gemm_grid_cap = 0;
 
 int high_launch_priority() {
   static int prio = [] {
@@ -71,16 +72,14 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 }
 
 template <int WMW, int WNW, int WTM, int WTN, int BK, int STAGES>
-__global__ void __launch_bounds__(WMW* WNW * 32, 1) gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
+__device__ __forceinline__ void gemm_tile(const GemmLaunch& L, const int tile, double* smem) {
   using C_ = Cfg<WMW, WNW, WTM, WTN, BK, STAGES>;
   constexpr int kThreads = C_::kThreads, kFM = C_::kFM, kFN = C_::kFN;
   constexpr int kALd = C_::kALd, kBLd = C_::kBLd, kAStage = C_::kAStage, kBStage = C_::kBStage;
-  extern __shared__ __align__(128) double smem[];
   double* sA = smem;
   double* sB = smem + STAGES * kAStage;
 
-  // ---- locate this CTA's (descriptor, batch item, tile) -------------------
-  const int tile = blockIdx.x;
+  // ---- locate this tile's (descriptor, batch item, tile) ------------------
   const GemmDesc* table = (L.count <= kGemmInline) ? L.inl : L.descs;
   int lo = 0, hi = L.count - 1;
   while (lo < hi) {  // last descriptor whose tile_begin <= tile
@@ -291,6 +290,17 @@ __global__ void __launch_bounds__(WMW* WNW * 32, 1) gemm_dmma_kernel(const __gri
   }
 }
 
+// Persistent over tiles: a launch may use fewer CTAs than tiles (the engine
+// caps GEMM grids to keep SMs free for the latency-bound leaf chains).
+template <int WMW, int WNW, int WTM, int WTN, int BK, int STAGES>
+__global__ void __launch_bounds__(WMW* WNW * 32, 1) gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
+  extern __shared__ __align__(128) double smem[];
+  for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
+    gemm_tile<WMW, WNW, WTM, WTN, BK, STAGES>(L, tile, smem);
+    __syncthreads();  // the next tile's prologue reuses the stage ring
+  }
+}
+
 // Variants (selected by BI_GEMM_VARIANT for tuning; default 2: 16 warps of
 // 32x32 -- measured best on every engine and leaf-update shape).
 #define BI_GEMM_VARIANTS(X)                \
@@ -360,10 +370,11 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
     if (!d_descs) return cudaErrorInvalidValue;
     L.descs = d_descs;
   }
+  const int grid = (g_gemm_grid_cap > 0 && g_gemm_grid_cap < total) ? g_gemm_grid_cap : total;
   switch (gemm_variant()) {
 #define BI_LAUNCH(id, a, b, c, d_, e_, f)                                                          \
   case id:                                                                                     \
-    e = launch_kernel(gemm_dmma_kernel<a, b, c, d_, e_, f>, dim3(total),                        \
+    e = launch_kernel(gemm_dmma_kernel<a, b, c, d_, e_, f>, dim3(grid),                         \
                       dim3(Cfg<a, b, c, d_, e_, f>::kThreads), Cfg<a, b, c, d_, e_, f>::kSmem, stream, 1u, \
                       L);                                                                      \
     break;

@@ -111,6 +111,16 @@ def main():
             o = np.empty((60, 60))
             f(R.diagonal_quad(m, 25), gj_sub, o)
             g[f"via_{nm}_60_25"] = o
+        for order, split in ((8, 4), (7, 3)):
+            m = well_conditioned(order, 10)
+            for nm, f in (("b", R.invert_via_b), ("c", R.invert_via_c), ("bc", R.invert_via_bc)):
+                o = np.empty((order, order))
+                f(R.counterdiagonal_quad(m, split), R.invert_small, o)
+                g[f"via_{nm}_{order}_{split}"] = o
+        perm2 = np.array([[0.0, 1.0], [1.0, 0.0]])
+        o = np.empty((2, 2))
+        g["fallback_perm2_name"] = np.array([R.invert_with_fallback(perm2, 1, o)])
+        g["fallback_perm2_out"] = o
         m = well_conditioned(4, 20)
         m[0, 0] = 0.0
         o = np.empty((4, 4))

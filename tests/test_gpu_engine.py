@@ -213,3 +213,66 @@ def test_reference_style_invert_sub_callable(bi):
     assert bi.invert_with_fallback(m, 15, out, invert_sub=sub) == "via_a"
     assert calls == [(15, 15), (25, 25)]
     assert oracle.residual_max(m, out) <= 1e-12
+
+
+def test_counterdiagonal_formulas(bi):
+    """schur.py:167-297 on the device (test_schur.py:95-137, 245-268)."""
+    perm2 = np.array([[0.0, 1.0], [1.0, 0.0]])
+    for f in (bi.invert_via_b, bi.invert_via_c):
+        out = np.empty((2, 2))
+        f(bi.counterdiagonal_quad(perm2, 1), bi.invert_small, out)
+        assert np.array_equal(out, perm2)
+    m = np.zeros((4, 4))
+    m[:2, 2:] = well_conditioned(2, 8)
+    m[2:, :2] = well_conditioned(2, 9)
+    for f in (bi.invert_via_b, bi.invert_via_c, bi.invert_via_bc):
+        out = np.empty((4, 4))
+        f(bi.counterdiagonal_quad(m, 2), bi.invert_small, out)
+        assert oracle.residual_max(m, out) <= 1e-12
+    m = well_conditioned(5, 11)
+    q = bi.counterdiagonal_quad(m, 2)
+    assert q.b.shape == (2, 2) and q.c.shape == (3, 3)
+    out = np.empty((5, 5))
+    bi.invert_via_b(q, bi.invert_small, out)
+    assert oracle.residual_max(m, out) <= 1e-9
+    assert bi.invert_with_fallback(perm2, 1, np.empty((2, 2))) == "via_b"
+    with pytest.raises(bi.AllPivotsSingular):
+        bi.invert_with_fallback(np.zeros((4, 4)), 2, np.empty((4, 4)))
+    for seed in range(20):  # all six formulas agree (test_schur.py:245-268)
+        m = well_conditioned(6, 3000 + seed)
+        outs = []
+        for f, mk in ((bi.invert_via_a, bi.diagonal_quad), (bi.invert_via_d, bi.diagonal_quad),
+                      (bi.invert_via_b, bi.counterdiagonal_quad), (bi.invert_via_c, bi.counterdiagonal_quad),
+                      (bi.invert_via_ad, bi.diagonal_quad), (bi.invert_via_bc, bi.counterdiagonal_quad)):
+            out = np.empty((6, 6))
+            f(mk(m, 3), bi.invert_small, out)
+            outs.append(out)
+        for o in outs[1:]:
+            assert np.max(np.abs(o - outs[0])) <= 6e-9
+    g = np.random.default_rng(5)
+    m = g.standard_normal((300, 300)) + 300 * np.eye(300)[::-1]  # counter-diagonal dominant
+    ref = oracle.gauss_jordan(m)
+    for f in (bi.invert_via_b, bi.invert_via_c, bi.invert_via_bc):
+        out = np.empty((300, 300))
+        f(bi.counterdiagonal_quad(m, 120), None, out)
+        assert oracle.rel_frob(out, ref) <= 1e-12
+    ref_b = np.empty((300, 300))
+    oracle.invert_via_b(m, 120, oracle.gj_sub, ref_b)
+    out = np.empty((300, 300))
+    bi.invert_via_b(bi.counterdiagonal_quad(m, 120), None, out)
+    assert oracle.rel_frob(out, ref_b) <= 1e-12
+
+
+def test_cfg3_full_scale_residual(bi):
+    """BASELINE config 3 at full size (n=6000, split 1000, rank-500 A11):
+    the automatic fallback must take via_d, and the residual must meet the
+    north-star bound ||MX - I||_F <= n eps cond(M) (cond ~ 1.1e7 -> 1.5e-5;
+    LAPACK itself reaches 1.8e-8)."""
+    from paper_2305_11103_b200.workloads import cfg3
+
+    m, split = cfg3()
+    out = np.empty_like(m)
+    assert bi.invert_with_fallback(m, split, out) == "via_d"
+    res = bi.residual_frobenius(m, out)
+    assert res <= 6000 * np.finfo(float).eps * 1.1e7, res
+    assert res <= 1e-6, res

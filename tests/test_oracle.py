@@ -119,6 +119,19 @@ def test_formulas_vs_golden():
     assert out.tobytes() == GOLDEN["fallback_kat_out"].tobytes()
 
 
+def test_counterdiagonal_formulas_vs_golden():
+    for order, split in ((8, 4), (7, 3)):
+        m = well_conditioned(order, 10)
+        for nm, f in (("b", oracle.invert_via_b), ("c", oracle.invert_via_c), ("bc", oracle.invert_via_bc)):
+            out = np.empty((order, order))
+            f(m, split, oracle.small_sub, out)
+            assert out.tobytes() == GOLDEN[f"via_{nm}_{order}_{split}"].tobytes(), (nm, order)
+    perm2 = np.array([[0.0, 1.0], [1.0, 0.0]])
+    out = np.empty((2, 2))
+    assert oracle.invert_with_fallback(perm2, 1, out) == str(GOLDEN["fallback_perm2_name"][0]) == "via_b"
+    assert np.array_equal(out, GOLDEN["fallback_perm2_out"])
+
+
 def test_cfg3_shape_vs_golden():
     from tests_golden_inputs import cfg3_small
 
