@@ -169,6 +169,7 @@ struct bi_engine {
   static constexpr int kMaxLanes = 8;
   void* inv_base[kMaxLanes] = {};
   int nlanes = 1;
+  int lane_priority[kMaxLanes] = {};
   int leaf_priority = 0;
   int gemm_cap = 0;  // engine GEMM grid cap (SMs left for the leaf chains)
   int zlo[kMaxLanes] = {}, zhi[kMaxLanes] = {};
@@ -461,12 +462,21 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   p += align256(e->info_ints * 4);
   BI_CUDA_TRY(init_attributes());
   {
-    const char* pe = getenv("BI_LEAF_PRIORITY");
-    e->leaf_priority = (pe && atoi(pe) == 0) ? 0 : high_launch_priority();
+    // BI_PRIORITY_MODE: 0 none, 1 lane order (lane 0 highest), 2 leaf kernels
+    // above GEMMs (default)
+    const char* pe = getenv("BI_PRIORITY_MODE");
+    const int mode = pe ? atoi(pe) : 2;
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    for (int l = 0; l < e->nlanes; ++l)
+      e->lane_priority[l] = (mode == 1 && e->nlanes > 1) ? std::min(greatest + l, least) : 0;
+    e->leaf_priority = mode == 2 ? greatest : 0;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const char* rs = getenv("BI_RESERVE_SMS");
+    // measured (profiles/r01_engine_overlap.txt): reserving 16 SMs from the
+    // engine GEMMs lets the leaf chains of the other lanes run alongside
     const int reserve = rs ? atoi(rs) : (e->nlanes > 1 ? 16 : 0);
     e->gemm_cap = (reserve > 0 && reserve < nsm) ? nsm - reserve : 0;
   }
@@ -550,12 +560,15 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
 
 static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cudaStream_t s, int mask,
                                 cudaEvent_t after_first = nullptr) {
+  // Lane priority: lane 0 highest.  The leading lane then runs as if alone
+  // and the others fill the SMs its latency-bound leaf phases leave idle.
+  PriorityScope lane_prio(e->lane_priority[lane]);
   for (int stepid = first; stepid <= last; ++stepid) {
     for (const Op& op : e->lane_ops[lane][stepid]) {
       if (!(mask & (op.kind == 0 ? 2 : 1))) continue;
       cudaError_t err;
       if (op.kind == 0) {
-        PriorityScope ps(e->leaf_priority);
+        PriorityScope leaf_prio(e->leaf_priority ? e->leaf_priority : g_launch_priority);
         err = launch_inv_group(e->invs[op.index].g, s);
       } else {
         GemmCapScope cap(e->gemm_cap);
@@ -670,7 +683,7 @@ static int run_impl(bi_engine* e, int first_step, int last_step, int use_graph, 
       return 3;
     }
     cudaGraphExec_t exec = nullptr;
-    cudaError_t err3 = cudaGraphInstantiate(&exec, graph, 0);
+    cudaError_t err3 = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(graph);
     BI_CUDA_TRY(err3);
     if (e->graphs.size() >= 16) {  // bound the cache

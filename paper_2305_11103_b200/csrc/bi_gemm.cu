@@ -301,8 +301,10 @@ __global__ void __launch_bounds__(WMW* WNW * 32, 1) gemm_dmma_kernel(const __gri
   }
 }
 
-// Variants (selected by BI_GEMM_VARIANT for tuning; default 2: 16 warps of
-// 32x32 -- measured best on every engine and leaf-update shape).
+// Variants (selected by BI_GEMM_VARIANT for tuning).  Default 4 = the TMA +
+// mbarrier kernel of bi_gemm_tma.cu (16 warps of 32x32), falling back to
+// variant 2 (cp.async, same warp layout) when operands are not 16-byte aligned
+// or a launch has more than kGemmInline descriptors.
 #define BI_GEMM_VARIANTS(X)                \
   X(0, 2, 4, 64, 32, 16, 4) /* 8 warps */  \
   X(1, 2, 4, 64, 32, 32, 3)                \
@@ -311,11 +313,15 @@ __global__ void __launch_bounds__(WMW* WNW * 32, 1) gemm_dmma_kernel(const __gri
 
 int g_variant = -1;
 
+}  // namespace
+bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t stream, cudaError_t* err);
+namespace {
+
 int gemm_variant() {
   if (g_variant < 0) {
     const char* v = getenv("BI_GEMM_VARIANT");
-    g_variant = v ? atoi(v) : 2;
-    if (g_variant < 0 || g_variant > 3) g_variant = 2;
+    g_variant = v ? atoi(v) : 4;
+    if (g_variant < 0 || g_variant > 4) g_variant = 4;
   }
   return g_variant;
 }
@@ -371,7 +377,11 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
     L.descs = d_descs;
   }
   const int grid = (g_gemm_grid_cap > 0 && g_gemm_grid_cap < total) ? g_gemm_grid_cap : total;
-  switch (gemm_variant()) {
+  if (gemm_variant() == 4) {
+    cudaError_t te = cudaSuccess;
+    if (launch_gemm_tma(h_descs, count, g_gemm_grid_cap, stream, &te)) return te;
+  }
+  switch (gemm_variant() == 4 ? 2 : gemm_variant()) {
 #define BI_LAUNCH(id, a, b, c, d_, e_, f)                                                          \
   case id:                                                                                     \
     e = launch_kernel(gemm_dmma_kernel<a, b, c, d_, e_, f>, dim3(grid),                         \

@@ -1,0 +1,308 @@
+// K1, TMA variant: D = [C] + sign * A * B with TMA-fed shared memory and an
+// mbarrier ring (no CTA-wide barrier in the main loop).
+//
+// sm_100a has no tcgen05 FP64 kind; the FP64 tensor path is DMMA.8x8x4
+// (mma.sync.m8n8k4.f64).  This variant feeds it the Blackwell way: one thread
+// issues cp.async.bulk.tensor (TMA) loads of 128-byte-swizzled tiles into a
+// 5-stage ring; full/empty mbarriers replace __syncthreads, so the 16 consumer
+// warps drift freely inside the ring and the per-thread address arithmetic of
+// cp.async disappears from the DMMA issue stream.
+//
+// Bank conflicts: with SWIZZLE_128B the natural m8n8k4 fragment pattern
+// conflicts 2-way.  The four k-slots of DMMA k-step s are therefore mapped to
+// the permuted k sets S0={0,3,12,15}, S1={2,1,14,13}, S2={4,7,8,11},
+// S3={6,5,10,9} of the 16-wide k-tile (the same permutation on A and B, i.e. a
+// reordering of the sum).  For both the A box ([m][k], 128 B rows) and the B
+// boxes ([k][16 n], 128 B rows) every half-warp then touches 16 distinct
+// 8-byte bank pairs.
+//
+// Replaces core._mm_acc / multiply / schur_accumulate (core.py:115-192) like
+// the cp.async variant in bi_gemm.cu; selected when every operand is 16-byte
+// aligned with even leading dimensions and the launch has <= 4 descriptors.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "bi_common.cuh"
+
+namespace bi {
+namespace {
+
+constexpr int kStages = 5;
+constexpr int kWarps = 16;  // 4 x 4 warps of 32 x 32
+constexpr int kThreads = kWarps * 32;
+constexpr int kBoxBBytes = 16 * 16 * 8;       // one B box: 16 k-rows x 16 doubles
+constexpr int kStageA = kBM * kBK * 8;        // 16 KB
+constexpr int kStageB = kBK * kBN * 8;        // 16 KB (8 boxes)
+constexpr int kStageBytes = kStageA + kStageB;
+constexpr int kSmem = kStages * kStageBytes + 1024;  // + alignment slack
+
+struct alignas(64) TmaLaunch {
+  CUtensorMap ta[kGemmInline];
+  CUtensorMap tb[kGemmInline];
+  GemmDesc d[kGemmInline];
+  int count, total_tiles;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int kslot(int s, int j) {
+  // S0={0,3,12,15} S1={2,1,14,13} S2={4,7,8,11} S3={6,5,10,9}, 4 bits per entry
+  constexpr unsigned long long tbl = 0x9a56b874de12fc30ull;
+  return (int)((tbl >> (4 * (s * 4 + j))) & 15);
+}
+
+struct TileCoord {
+  int desc, bz, m0, n0;
+};
+
+__device__ __forceinline__ TileCoord locate(const TmaLaunch& L, int tile) {
+  int lo = 0, hi = L.count - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (L.d[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
+  }
+  const GemmDesc& d = L.d[lo];
+  const int local = tile - d.tile_begin;
+  const int per = d.tiles_m * d.tiles_n;
+  const int bz = local / per;
+  const int rem = local - bz * per;
+  const int tm = rem / d.tiles_n;
+  return TileCoord{lo, bz, tm * kBM, (rem - tm * d.tiles_n) * kBN};
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_constant__ TmaLaunch L) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int fr = lane >> 2, fc = lane & 3;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // per-thread fragment offsets (bytes) for the 4 k-steps
+  int aoff[4], boff[4][2];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int k = kslot(s, fc);
+    aoff[s] = ((((k >> 1) ^ fr) & 7) << 4) + ((k & 1) << 3);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      boff[s][h] = k * 128 + (((h * 4 + (fr >> 1)) ^ (k & 7)) << 4) + ((fr & 1) << 3);
+  }
+
+  unsigned prod_it = 0;  // producer's k-tile counter (thread 0 only)
+  unsigned cons_it = 0;  // consumers' k-tile counter
+  auto issue = [&](const TileCoord& tc, int kt) {
+    const int stage = prod_it % kStages;
+    if (prod_it >= (unsigned)kStages) mbar_wait(&empty[stage], ((prod_it / kStages) - 1) & 1);
+    uint8_t* sa = smem + stage * kStageBytes;
+    uint8_t* sb = sa + kStageA;
+    mbar_expect_tx(&full[stage], kStageBytes);
+    tma_load_3d(sa, &L.ta[tc.desc], &full[stage], kt * kBK, tc.m0, tc.bz);
+#pragma unroll
+    for (int j = 0; j < kBN / 16; ++j)
+      tma_load_3d(sb + j * kBoxBBytes, &L.tb[tc.desc], &full[stage], tc.n0 + 16 * j, kt * kBK, tc.bz);
+    ++prod_it;
+  };
+
+  for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
+    const TileCoord tc = locate(L, tile);
+    const GemmDesc& d = L.d[tc.desc];
+    const int KT = (d.K + kBK - 1) / kBK;
+    if (tid == 0) {
+      for (int kt = 0; kt < KT && kt < kStages - 1; ++kt) issue(tc, kt);
+    }
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+      if (tid == 0 && kt + kStages - 1 < KT) issue(tc, kt + kStages - 1);
+      const int stage = cons_it % kStages;
+      mbar_wait(&full[stage], (cons_it / kStages) & 1);
+      const uint8_t* sa = smem + stage * kStageBytes + (wm * 32 + fr) * 128;
+      const uint8_t* sb = smem + stage * kStageBytes + kStageA + (wn * 2) * kBoxBBytes;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = *reinterpret_cast<const double*>(sa + i * 8 * 128 + aoff[s]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          bf[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * kBoxBBytes + boff[s][j & 1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      ++cons_it;
+    }
+
+    // ---- epilogue: D = [C] + sign * acc (C loads first; C may alias D)
+    const int mrem = d.M - tc.m0, nrem = d.N - tc.n0;
+    const double* C = d.C ? d.C + tc.bz * d.sC : nullptr;
+    double* D = d.D + tc.bz * d.sD;
+    const double sgn = d.neg ? -1.0 : 1.0;
+    auto pcol = [&](int g) { return g < d.skip_at ? g : g + d.skip_len; };
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[i][j][0] *= sgn;
+        acc[i][j][1] *= sgn;
+      }
+    if (C) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = wm * 32 + i * 8 + fr;
+        const int64_t row = tc.m0 + r;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int cl = wn * 32 + j * 8 + 2 * fc;
+          if (r >= mrem || cl >= nrem) continue;
+          const int p0 = pcol(tc.n0 + cl), p1 = pcol(tc.n0 + cl + 1);
+          const double* cp = C + row * d.ldc + p0;
+          if (cl + 1 < nrem && p1 == p0 + 1 && (((uintptr_t)cp) & 15) == 0) {
+            const double2 cv = __ldg(reinterpret_cast<const double2*>(cp));
+            acc[i][j][0] += cv.x;
+            acc[i][j][1] += cv.y;
+          } else {
+            acc[i][j][0] += cp[0];
+            if (cl + 1 < nrem) acc[i][j][1] += C[row * d.ldc + p1];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = wm * 32 + i * 8 + fr;
+      const int64_t row = tc.m0 + r;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cl = wn * 32 + j * 8 + 2 * fc;
+        if (r >= mrem || cl >= nrem) continue;
+        const int p0 = pcol(tc.n0 + cl), p1 = pcol(tc.n0 + cl + 1);
+        double* dp = D + row * d.ldd + p0;
+        if (cl + 1 < nrem && p1 == p0 + 1 && (((uintptr_t)dp) & 15) == 0) {
+          *reinterpret_cast<double2*>(dp) = make_double2(acc[i][j][0], acc[i][j][1]);
+        } else {
+          dp[0] = acc[i][j][0];
+          if (cl + 1 < nrem) D[row * d.ldd + p1] = acc[i][j][1];
+        }
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_tma_once;
+cudaError_t g_tma_err = cudaSuccess;
+
+cudaError_t tma_init() {
+  std::call_once(g_tma_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) {
+      g_tma_err = e != cudaSuccess ? e : cudaErrorNotSupported;
+      return;
+    }
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  });
+  return g_tma_err;
+}
+
+bool encode_3d(CUtensorMap* map, const double* base, uint64_t inner, uint64_t outer, uint64_t batch, int64_t ld,
+               int64_t bstride, uint32_t box_inner, uint32_t box_outer) {
+  cuuint64_t dims[3] = {inner, outer, batch};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)(batch > 1 ? bstride : ld * (int64_t)outer) * 8};
+  cuuint32_t box[3] = {box_inner, box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// Returns true when the launch was issued with the TMA kernel; false when the
+// descriptors do not qualify (caller falls back to the cp.async kernel).
+bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t stream, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (count <= 0 || count > kGemmInline) return false;
+  if (tma_init() != cudaSuccess) return false;
+  TmaLaunch L;
+  std::memset(&L, 0, sizeof(L));
+  L.count = count;
+  int total = 0;
+  for (int i = 0; i < count; ++i) {
+    const GemmDesc& d = h[i];
+    const bool ok = (((uintptr_t)d.A | (uintptr_t)d.B) & 15) == 0 && ((d.lda | d.ldb) & 1) == 0 &&
+                    (d.batch <= 1 || ((d.sA | d.sB) & 1) == 0) && d.sA >= 0 && d.sB >= 0 && d.K > 0;
+    if (!ok) return false;
+    const uint64_t batch = d.batch > 0 ? (uint64_t)d.batch : 1;
+    if (!encode_3d(&L.ta[i], d.A, (uint64_t)d.K, (uint64_t)d.M, batch, d.lda, d.sA, kBK, kBM)) return false;
+    if (!encode_3d(&L.tb[i], d.B, (uint64_t)d.N, (uint64_t)d.K, batch, d.ldb, d.sB, 16, kBK)) return false;
+    L.d[i] = d;
+    total = d.tile_begin + ((d.M <= 0 || d.N <= 0 || d.batch <= 0) ? 0 : d.tiles_m * d.tiles_n * d.batch);
+  }
+  L.total_tiles = total;
+  if (total == 0) return true;
+  const int grid = (grid_cap > 0 && grid_cap < total) ? grid_cap : total;
+  *err = launch_kernel(gemm_tma_kernel, dim3(grid), dim3(kThreads), (size_t)kSmem, stream, 1u, L);
+  return true;
+}
+
+}  // namespace bi
