@@ -82,6 +82,9 @@ static std::vector<GemmDesc> merge_descs(const std::vector<GemmDesc>& in) {
                         p.skip_at == d.skip_at && (p.C == nullptr) == (d.C == nullptr);
       if (same) {
         const int64_t dA = d.A - p.A, dB = d.B - p.B, dD = d.D - p.D, dC = d.C ? d.C - p.C : 0;
+        // TMA batch strides are unsigned: keep descriptors apart rather than
+        // produce a negative A/B stride (the launch would lose the TMA path)
+        if (dA < 0 || dB < 0) goto no_merge;
         if (p.batch == 1) {
           p.sA = dA;
           p.sB = dB;
@@ -97,6 +100,7 @@ static std::vector<GemmDesc> merge_descs(const std::vector<GemmDesc>& in) {
         }
       }
     }
+  no_merge:
     GemmDesc c = d;
     c.batch = 1;
     c.sA = c.sB = c.sC = c.sD = 0;

@@ -25,18 +25,17 @@
 #include <cstring>
 #include <mutex>
 
-#include "bi_common.cuh"
+#include "bi_gemm_core.cuh"
 
 namespace bi {
 namespace {
 
 constexpr int kStages = 5;
-constexpr int kWarps = 16;  // 4 x 4 warps of 32 x 32
-constexpr int kThreads = kWarps * 32;
-constexpr int kBoxBBytes = 16 * 16 * 8;       // one B box: 16 k-rows x 16 doubles
-constexpr int kStageA = kBM * kBK * 8;        // 16 KB
-constexpr int kStageB = kBK * kBN * 8;        // 16 KB (8 boxes)
-constexpr int kStageBytes = kStageA + kStageB;
+constexpr int kWarps = kK1Warps;
+constexpr int kThreads = kK1Threads;
+constexpr int kBoxBBytes = kK1BoxB;
+constexpr int kStageA = kK1StageA;
+constexpr int kStageBytes = kK1Stage;
 constexpr int kSmem = kStages * kStageBytes + 1024;  // + alignment slack
 
 struct alignas(64) TmaLaunch {
@@ -77,37 +76,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(c[0]), "+d"(c[1])
-      : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ int kslot(int s, int j) {
-  // S0={0,3,12,15} S1={2,1,14,13} S2={4,7,8,11} S3={6,5,10,9}, 4 bits per entry
-  constexpr unsigned long long tbl = 0x9a56b874de12fc30ull;
-  return (int)((tbl >> (4 * (s * 4 + j))) & 15);
-}
-
-struct TileCoord {
-  int desc, bz, m0, n0;
-};
-
-__device__ __forceinline__ TileCoord locate(const TmaLaunch& L, int tile) {
-  int lo = 0, hi = L.count - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (L.d[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
-  }
-  const GemmDesc& d = L.d[lo];
-  const int local = tile - d.tile_begin;
-  const int per = d.tiles_m * d.tiles_n;
-  const int bz = local / per;
-  const int rem = local - bz * per;
-  const int tm = rem / d.tiles_n;
-  return TileCoord{lo, bz, tm * kBM, (rem - tm * d.tiles_n) * kBN};
-}
-
 __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_constant__ TmaLaunch L) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -125,20 +93,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_cons
   }
   __syncthreads();
 
-  // per-thread fragment offsets (bytes) for the 4 k-steps
-  int aoff[4], boff[4][2];
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int k = kslot(s, fc);
-    aoff[s] = ((((k >> 1) ^ fr) & 7) << 4) + ((k & 1) << 3);
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      boff[s][h] = k * 128 + (((h * 4 + (fr >> 1)) ^ (k & 7)) << 4) + ((fr & 1) << 3);
-  }
+  K1Frag f;
+  k1_frag_init(f, fr, fc);
 
   unsigned prod_it = 0;  // producer's k-tile counter (thread 0 only)
   unsigned cons_it = 0;  // consumers' k-tile counter
-  auto issue = [&](const TileCoord& tc, int kt) {
+  auto issue = [&](const K1Tile& tc, int kt) {
     const int stage = prod_it % kStages;
     if (prod_it >= (unsigned)kStages) mbar_wait(&empty[stage], ((prod_it / kStages) - 1) & 1);
     uint8_t* sa = smem + stage * kStageBytes;
@@ -152,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_cons
   };
 
   for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
-    const TileCoord tc = locate(L, tile);
+    const K1Tile tc = k1_locate(L.d, L.count, tile);
     const GemmDesc& d = L.d[tc.desc];
     const int KT = (d.K + kBK - 1) / kBK;
     if (tid == 0) {
@@ -168,79 +128,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_cons
       if (tid == 0 && kt + kStages - 1 < KT) issue(tc, kt + kStages - 1);
       const int stage = cons_it % kStages;
       mbar_wait(&full[stage], (cons_it / kStages) & 1);
-      const uint8_t* sa = smem + stage * kStageBytes + (wm * 32 + fr) * 128;
-      const uint8_t* sb = smem + stage * kStageBytes + kStageA + (wn * 2) * kBoxBBytes;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        double af[4], bf[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = *reinterpret_cast<const double*>(sa + i * 8 * 128 + aoff[s]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          bf[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * kBoxBBytes + boff[s][j & 1]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
-      }
+      k1_compute(smem + stage * kStageBytes, f, wm, wn, fr, acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       ++cons_it;
     }
 
-    // ---- epilogue: D = [C] + sign * acc (C loads first; C may alias D)
-    const int mrem = d.M - tc.m0, nrem = d.N - tc.n0;
-    const double* C = d.C ? d.C + tc.bz * d.sC : nullptr;
-    double* D = d.D + tc.bz * d.sD;
-    const double sgn = d.neg ? -1.0 : 1.0;
-    auto pcol = [&](int g) { return g < d.skip_at ? g : g + d.skip_len; };
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        acc[i][j][0] *= sgn;
-        acc[i][j][1] *= sgn;
-      }
-    if (C) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = wm * 32 + i * 8 + fr;
-        const int64_t row = tc.m0 + r;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int cl = wn * 32 + j * 8 + 2 * fc;
-          if (r >= mrem || cl >= nrem) continue;
-          const int p0 = pcol(tc.n0 + cl), p1 = pcol(tc.n0 + cl + 1);
-          const double* cp = C + row * d.ldc + p0;
-          if (cl + 1 < nrem && p1 == p0 + 1 && (((uintptr_t)cp) & 15) == 0) {
-            const double2 cv = __ldg(reinterpret_cast<const double2*>(cp));
-            acc[i][j][0] += cv.x;
-            acc[i][j][1] += cv.y;
-          } else {
-            acc[i][j][0] += cp[0];
-            if (cl + 1 < nrem) acc[i][j][1] += C[row * d.ldc + p1];
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = wm * 32 + i * 8 + fr;
-      const int64_t row = tc.m0 + r;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int cl = wn * 32 + j * 8 + 2 * fc;
-        if (r >= mrem || cl >= nrem) continue;
-        const int p0 = pcol(tc.n0 + cl), p1 = pcol(tc.n0 + cl + 1);
-        double* dp = D + row * d.ldd + p0;
-        if (cl + 1 < nrem && p1 == p0 + 1 && (((uintptr_t)dp) & 15) == 0) {
-          *reinterpret_cast<double2*>(dp) = make_double2(acc[i][j][0], acc[i][j][1]);
-        } else {
-          dp[0] = acc[i][j][0];
-          if (cl + 1 < nrem) D[row * d.ldd + p1] = acc[i][j][1];
-        }
-      }
-    }
+    k1_epilogue(d, tc.bz, tc.m0, tc.n0, wm, wn, fr, fc, acc);
   }
 }
 

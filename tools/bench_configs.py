@@ -1,0 +1,135 @@
+"""Time the other BASELINE.json configs on one B200 (not the driver's bench
+line; recorded under profiles/).  Each run is verified by the on-device
+residual ||A X - I||_F (K1 + K4).
+
+  cfg1  n=512, (256, 256): invertor_inplace_by_a and run_inversion
+  cfg3  n=6000, split 1000, singular A11: invert_with_fallback -> via_d
+  cfg4  n=16384, 64 x 256 blocks: run_inversion step engine (127 steps)
+  cfg5  n=65536, 256 x 256 blocks (--cfg5): run_inversion on ONE GPU
+        (~138 GB of device state); input drawn on the device (torch
+        Philox, seed 5) with the config's distribution, N(0,1)/256 + 4I
+"""
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2305_11103_b200 as bi  # noqa: E402
+from paper_2305_11103_b200 import workloads  # noqa: E402
+from paper_2305_11103_b200.core import _residual_device  # noqa: E402
+
+
+def events():
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def time_engine(eng, reps):
+    eng.run()
+    eng.check()
+    torch.cuda.synchronize()
+    a, b = events()
+    a.record()
+    for _ in range(reps):
+        eng.run()
+    b.record()
+    torch.cuda.synchronize()
+    eng.check()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg5", action="store_true")
+    ap.add_argument("--skip", default="")
+    args = ap.parse_args()
+    out = {}
+    skip = set(args.skip.split(","))
+
+    if "cfg1" not in skip:
+        m, sizes = workloads.cfg1()
+        x = m.copy()
+        bi.invertor_inplace_by_a(x)
+        t0 = time.perf_counter()
+        for _ in range(5):
+            x = m.copy()
+            bi.invertor_inplace_by_a(x)
+        t_inplace = (time.perf_counter() - t0) / 5
+        eng = bi.DeviceEngine(sizes, 1)
+        eng.load(m)
+        ms = time_engine(eng, 20)
+        fro, _ = _residual_device(eng.M, eng.Minv, batch=True)
+        out["cfg1"] = {"inplace_by_a_s_e2e": t_inplace, "run_inversion_device_ms": ms,
+                       "tflops_nominal_device": 2 * 512**3 / (ms * 1e-3) / 1e12,
+                       "residual_fro": float(fro[0]), "residual_fro_inplace": bi.residual_frobenius(m, x)}
+        print("cfg1", out["cfg1"], flush=True)
+
+    if "cfg3" not in skip:
+        m, split = workloads.cfg3()
+        res = np.empty_like(m)
+        bi.invert_with_fallback(m, split, res)
+        from paper_2305_11103_b200 import _lib
+        from paper_2305_11103_b200.schur import schur2x2_device
+
+        md = _lib.to_device(m)
+        od = _lib.empty_matrix(6000, 6000)
+        schur2x2_device("D", md, split, od)
+        torch.cuda.synchronize()
+        a, b = events()
+        a.record()
+        for _ in range(3):
+            schur2x2_device("D", md, split, od)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 3
+        out["cfg3"] = {"via": bi.invert_with_fallback(m, split, res), "via_d_device_ms": ms,
+                       "tflops_nominal": 2 * 6000**3 / (ms * 1e-3) / 1e12,
+                       "residual_fro": bi.residual_frobenius(m, res)}
+        print("cfg3", out["cfg3"], flush=True)
+
+    if "cfg4" not in skip:
+        m, sizes = workloads.cfg4()
+        eng = bi.DeviceEngine(sizes, 1)
+        eng.load(m)
+        del m
+        ms = time_engine(eng, 2)
+        fro, _ = _residual_device(eng.M, eng.Minv, batch=True)
+        c = eng.counters()
+        out["cfg4"] = {"run_inversion_device_ms": ms, "tflops_nominal": 2 * 16384**3 / (ms * 1e-3) / 1e12,
+                       "tflops_algorithmic": (c["gemm_flops"] + c["leaf_flops"]) / (ms * 1e-3) / 1e12,
+                       "residual_fro": float(fro[0])}
+        print("cfg4", out["cfg4"], flush=True)
+        del eng
+        torch.cuda.empty_cache()
+
+    if args.cfg5:
+        n = 65536
+        sizes = [256] * 256
+        eng = bi.DeviceEngine(sizes, 1)
+        g = torch.Generator(device="cuda")
+        g.manual_seed(5)
+        for r0 in range(0, n, 4096):  # draw row chunks straight into M
+            blk = torch.randn((4096, n), generator=g, dtype=torch.float64, device="cuda")
+            blk.div_(256.0)
+            eng.M[0, r0:r0 + 4096].copy_(blk)
+            del blk
+        idx = torch.arange(n, device="cuda")
+        eng.M[0, idx, idx] += 4.0
+        torch.cuda.synchronize()
+        ms = time_engine(eng, 1)
+        fro, mx = _residual_device(eng.M, eng.Minv, batch=True)
+        out["cfg5"] = {"run_inversion_device_s": ms / 1e3, "tflops_nominal": 2 * n**3 / (ms * 1e-3) / 1e12,
+                       "residual_fro": float(fro[0]), "residual_max": float(mx[0]),
+                       "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
+                       "input": "device-drawn N(0,1)/256 + 4I (torch Philox, seed 5)"}
+        print("cfg5", out["cfg5"], flush=True)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
