@@ -92,7 +92,9 @@ int bi_inv_batched(int count, int64_t n,
  *   bi_engine_counters -> OpCounters semantics of the executed steps
  *                          (engine.py:317, 344-345, 411):
  *                          out[0]=multiplies out[1]=inversions out[2]=reductions
- *                          out[3]=gemm flops (algorithmic) out[4]=leaf flops.
+ *                          out[3]=gemm flops (algorithmic) out[4]=leaf flops
+ *                          out[5]=gemm bytes (algorithmic: each operand read
+ *                          once, each output written once).
  * ---------------------------------------------------------------------- */
 typedef struct bi_engine bi_engine;
 int bi_engine_create(bi_engine** out, int nblocks, const int64_t* sizes, int batch);
@@ -120,7 +122,7 @@ int bi_engine_run_phase(bi_engine* e, int first_step, int last_step, int mask, v
 /* Kernel launches of steps [first, last]: out[0] total, out[1] K1 (engine
  * GEMMs + leaf trailing updates), out[2] other K3 kernels. */
 int bi_engine_launches(const bi_engine* e, int first_step, int last_step, int64_t out[3]);
-int bi_engine_counters(const bi_engine* e, int first_step, int last_step, double out[5]);
+int bi_engine_counters(const bi_engine* e, int first_step, int last_step, double out[6]);
 /* T-set access for step-state parity: pointer + ld of the level-`level`
  * provisional square of quad `quad` of matrix `matrix` (S_D at A's
  * position, R at B's, L at C's, S_A at D's; storage.py:166-262). */

@@ -76,6 +76,17 @@ int finalize_descs(GemmDesc* d, int count);
 // Launch on `stream`. `d_descs` may be null when count <= kGemmInline.
 cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int count,
                         cudaStream_t stream);
+// One descriptor on 64 x 64 tiles (latency path; same summation order).
+cudaError_t launch_gemm_small(const GemmDesc& h, cudaStream_t stream);
+
+// Preferred L1/shared carveout (percent) applied to every kernel of the
+// library, from BI_CARVEOUT (default -1 = driver default).
+int carveout_percent();
+template <typename K>
+cudaError_t set_carveout(K kernel) {
+  const int c = carveout_percent();
+  return c < 0 ? cudaSuccess : cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+}
 
 // ---------------------------------------------------------------------------
 // K3 batched pivoted Gauss-Jordan, one group of equal-order blocks.

@@ -789,10 +789,10 @@ extern "C" int bi_engine_status(bi_engine* e, int* fail_step, int* fail_quad, in
   return 0;
 }
 
-extern "C" int bi_engine_counters(const bi_engine* e, int first_step, int last_step, double out[5]) {
+extern "C" int bi_engine_counters(const bi_engine* e, int first_step, int last_step, double out[6]) {
   BI_REQUIRE(e && out, "null argument");
   BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps, "stepid outside 1..N_s");
-  double mult = 0, invs = 0, red = 0, gflops = 0, lflops = 0;
+  double mult = 0, invs = 0, red = 0, gflops = 0, lflops = 0, gbytes = 0;
   const auto& off = e->off;
   for (int stepid = first_step; stepid <= last_step; ++stepid) {
     StepAct a;
@@ -812,12 +812,16 @@ extern "C" int bi_engine_counters(const bi_engine* e, int first_step, int last_s
         mult += 2;  // engine.py:344-345
         red += 2;
         gflops += 2.0 * (ha * ha * hd + hd * hd * ha + ha * hd * ha + hd * ha * hd);
+        // R, L: read A^-1 / D^-1 and B / C, write R / L; S_D, S_A: read B L + A / C R + D, write
+        gbytes += 8.0 * ((ha * ha + 2 * ha * hd) + (hd * hd + 2 * ha * hd) + (2 * ha * hd + 2 * ha * ha) +
+                         (2 * ha * hd + 2 * hd * hd));
       });
     } else if (a.kind == 2) {
       for (int lv = 1; lv <= a.depth; ++lv)
         quads(lv, [&](double ha, double hd) {
           mult += 2;  // engine.py:411
           gflops += 2.0 * (hd * ha * ha + ha * hd * hd);
+          gbytes += 8.0 * ((2 * ha * hd + ha * ha) + (2 * ha * hd + hd * hd));  // down, up
         });
     }
   }
@@ -826,6 +830,7 @@ extern "C" int bi_engine_counters(const bi_engine* e, int first_step, int last_s
   out[2] = red;
   out[3] = gflops * e->Z;
   out[4] = lflops * e->Z;
+  out[5] = gbytes * e->Z;
   return 0;
 }
 

@@ -29,6 +29,14 @@ namespace bi {
 thread_local int g_launch_priority = 0;
 thread_local int g_gemm_grid_cap = 0;
 
+int carveout_percent() {
+  static const int v = [] {
+    const char* e = getenv("BI_CARVEOUT");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+
 int high_launch_priority() {
   static int prio = [] {
     int least = 0, greatest = 0;
@@ -43,7 +51,21 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
 namespace {
 
 constexpr int kStages = 4;
-constexpr int kSmem = kStages * kK1Stage + 1024;
+
+// Tile configurations of the cp.async feeder: TM x TN CTA tile of 32 x 32
+// warp tiles.  128 x 128 (16 warps) is the throughput tile; 64 x 64 (4 warps)
+// is the latency tile for the small trailing updates of K3, where one FP64 SM
+// (~250 GF/s) would otherwise spend >4 us on a single 128 x 128 x 32 tile.
+// Both sum every element in the same order (same k-tile / k-slot sequence per
+// warp tile), so results do not depend on the tile shape.
+template <int TM, int TN>
+struct K1Cfg {
+  static constexpr int kWN = TN / 32;
+  static constexpr int kThreads = (TM / 32) * kWN * 32;
+  static constexpr int kStageA = TM * kBK * 8;
+  static constexpr int kStage = kStageA + kBK * TN * 8;
+  static constexpr int kSmem = kStages * kStage + 1024;
+};
 
 __device__ __forceinline__ void cp_async16(uint8_t* smem, const double* gmem, int src_bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -59,10 +81,13 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+template <int TM, int TN>
 __device__ __forceinline__ void gemm_tile(const GemmLaunch& L, const int tile, uint8_t* smem, const K1Frag& f,
                                           int wm, int wn, int fr, int fc) {
+  using Cfg = K1Cfg<TM, TN>;
+  constexpr int kThr = Cfg::kThreads;
   const GemmDesc* table = (L.count <= kGemmInline) ? L.inl : L.descs;
-  const K1Tile tc = k1_locate(table, L.count, tile);
+  const K1Tile tc = k1_locate<TM, TN>(table, L.count, tile);
   const GemmDesc& d = table[tc.desc];
   const int mrem = d.M - tc.m0, nrem = d.N - tc.n0, K = d.K;
   const int64_t lda = d.lda, ldb = d.ldb;
@@ -70,15 +95,18 @@ __device__ __forceinline__ void gemm_tile(const GemmLaunch& L, const int tile, u
   const double* __restrict__ B = d.B + tc.bz * d.sB + tc.n0;
   const bool al16 = ((((uintptr_t)A) | ((uintptr_t)B)) & 15) == 0 && ((lda | ldb) & 1) == 0;
   const int tid = threadIdx.x;
+  auto b_chunk = [&](int k, int cc) {  // byte offset of B chunk (k-row k, 16-byte chunk cc)
+    return Cfg::kStageA + (cc >> 3) * kK1BoxB + k * 128 + (((cc & 7) ^ (k & 7)) << 4);
+  };
 
   // copy one k-tile into a stage of the swizzled layout
   auto load_stage = [&](int stage, int kt) {
     const int k0 = kt * kBK;
-    uint8_t* st = smem + stage * kK1Stage;
+    uint8_t* st = smem + stage * Cfg::kStage;
     if (al16) {
 #pragma unroll
-      for (int i = 0; i < (kBM * kBK / 2) / kK1Threads; ++i) {  // A: 128 rows x 8 chunks
-        const int q = tid + i * kK1Threads;
+      for (int i = 0; i < (TM * kBK / 2) / kThr; ++i) {  // A: TM rows x 8 chunks
+        const int q = tid + i * kThr;
         const int row = q >> 3, c = q & 7, kk = k0 + 2 * c;
         int bytes = 0;
         const double* src = A;
@@ -89,50 +117,48 @@ __device__ __forceinline__ void gemm_tile(const GemmLaunch& L, const int tile, u
         cp_async16(st + row * 128 + ((c ^ (row & 7)) << 4), src, bytes);
       }
 #pragma unroll
-      for (int i = 0; i < (kBK * kBN / 2) / kK1Threads; ++i) {  // B: 16 rows x 64 chunks
-        const int q = tid + i * kK1Threads;
-        const int k = q >> 6, cc = q & 63, kk = k0 + k;
+      for (int i = 0; i < (kBK * TN / 2) / kThr; ++i) {  // B: 16 rows x TN/2 chunks
+        const int q = tid + i * kThr;
+        const int k = q / (TN / 2), cc = q % (TN / 2), kk = k0 + k;
         int bytes = 0;
         const double* src = B;
         if (kk < K && 2 * cc < nrem) {
           bytes = min(2, nrem - 2 * cc) * 8;
           src = B + (int64_t)kk * ldb + 2 * cc;
         }
-        cp_async16(st + kK1StageA + (cc >> 3) * kK1BoxB + k * 128 + (((cc & 7) ^ (k & 7)) << 4), src, bytes);
+        cp_async16(st + b_chunk(k, cc), src, bytes);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < (kBM * kBK) / kK1Threads; ++i) {
-        const int e = tid + i * kK1Threads;
+      for (int i = 0; i < (TM * kBK) / kThr; ++i) {
+        const int e = tid + i * kThr;
         const int row = e >> 4, kc = e & 15, kk = k0 + kc;
         const bool ok = row < mrem && kk < K;
         cp_async8(st + k1_a_off(row, kc), ok ? A + (int64_t)row * lda + kk : A, ok ? 8 : 0);
       }
 #pragma unroll
-      for (int i = 0; i < (kBK * kBN) / kK1Threads; ++i) {
-        const int e = tid + i * kK1Threads;
-        const int k = e >> 7, n = e & 127, kk = k0 + k;
+      for (int i = 0; i < (kBK * TN) / kThr; ++i) {
+        const int e = tid + i * kThr;
+        const int k = e / TN, n = e % TN, kk = k0 + k;
         const bool ok = kk < K && n < nrem;
-        cp_async8(st + k1_b_off(k, n), ok ? B + (int64_t)kk * ldb + n : B, ok ? 8 : 0);
+        cp_async8(st + b_chunk(k, n >> 1) + ((n & 1) << 3), ok ? B + (int64_t)kk * ldb + n : B, ok ? 8 : 0);
       }
     }
   };
 
-  // interior tiles with aligned operands: per-thread source pointers advance
-  // by one k-tile per stage, no bounds checks
-  const bool fast = al16 && mrem >= kBM && nrem >= kBN && (K % kBK) == 0;
+  // interior tiles with aligned operands: no bounds checks
+  const bool fast = al16 && mrem >= TM && nrem >= TN && (K % kBK) == 0;
   auto load_fast = [&](int stage, int kt) {
-    uint8_t* st = smem + stage * kK1Stage;
+    uint8_t* st = smem + stage * Cfg::kStage;
 #pragma unroll
-    for (int i = 0; i < (kBM * kBK / 2) / kK1Threads; ++i) {
-      const int q = tid + i * kK1Threads, row = q >> 3, c = q & 7;
+    for (int i = 0; i < (TM * kBK / 2) / kThr; ++i) {
+      const int q = tid + i * kThr, row = q >> 3, c = q & 7;
       cp_async16(st + row * 128 + ((c ^ (row & 7)) << 4), A + (int64_t)row * lda + kt * kBK + 2 * c, 16);
     }
 #pragma unroll
-    for (int i = 0; i < (kBK * kBN / 2) / kK1Threads; ++i) {
-      const int q = tid + i * kK1Threads, k = q >> 6, cc = q & 63;
-      cp_async16(st + kK1StageA + (cc >> 3) * kK1BoxB + k * 128 + (((cc & 7) ^ (k & 7)) << 4),
-                 B + (int64_t)(kt * kBK + k) * ldb + 2 * cc, 16);
+    for (int i = 0; i < (kBK * TN / 2) / kThr; ++i) {
+      const int q = tid + i * kThr, k = q / (TN / 2), cc = q % (TN / 2);
+      cp_async16(st + b_chunk(k, cc), B + (int64_t)(kt * kBK + k) * ldb + 2 * cc, 16);
     }
   };
 
@@ -158,20 +184,21 @@ __device__ __forceinline__ void gemm_tile(const GemmLaunch& L, const int tile, u
       if (fast) load_fast(nk % kStages, nk); else load_stage(nk % kStages, nk);
     }
     cp_async_commit();
-    k1_compute(smem + (kt % kStages) * kK1Stage, f, wm, wn, fr, acc);
+    k1_compute<Cfg::kStageA>(smem + (kt % kStages) * Cfg::kStage, f, wm, wn, fr, acc);
   }
-  k1_epilogue(d, tc.bz, tc.m0, tc.n0, wm, wn, fr, fc, acc);
+  k1_epilogue<TM, TN>(d, tc.bz, tc.m0, tc.n0, wm, wn, fr, fc, acc);
 }
 
-__global__ void __launch_bounds__(kK1Threads, 1) gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
+template <int TM, int TN>
+__global__ void __launch_bounds__(K1Cfg<TM, TN>::kThreads) gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = warp >> 2, wn = warp & 3, fr = lane >> 2, fc = lane & 3;
+  const int wm = warp / K1Cfg<TM, TN>::kWN, wn = warp % K1Cfg<TM, TN>::kWN, fr = lane >> 2, fc = lane & 3;
   K1Frag f;
   k1_frag_init(f, fr, fc);
   for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
-    gemm_tile(L, tile, smem, f, wm, wn, fr, fc);
+    gemm_tile<TM, TN>(L, tile, smem, f, wm, wn, fr, fc);
     cp_async_wait<0>();
     __syncthreads();  // the next tile's prologue reuses the stage ring
   }
@@ -204,7 +231,13 @@ int finalize_descs(GemmDesc* d, int count) {
 
 cudaError_t gemm_init_attributes() {
   std::call_once(g_attr_once, [] {
-    g_attr_err = cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    g_attr_err = cudaFuncSetAttribute(gemm_dmma_kernel<kBM, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      K1Cfg<kBM, kBN>::kSmem);
+    if (g_attr_err == cudaSuccess)
+      g_attr_err = cudaFuncSetAttribute(gemm_dmma_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        K1Cfg<64, 64>::kSmem);
+    if (g_attr_err == cudaSuccess) g_attr_err = set_carveout(gemm_dmma_kernel<kBM, kBN>);
+    if (g_attr_err == cudaSuccess) g_attr_err = set_carveout(gemm_dmma_kernel<64, 64>);
   });
   return g_attr_err;
 }
@@ -232,7 +265,26 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
     L.descs = d_descs;
   }
   const int grid = (g_gemm_grid_cap > 0 && g_gemm_grid_cap < total) ? g_gemm_grid_cap : total;
-  return launch_kernel(gemm_dmma_kernel, dim3(grid), dim3(kK1Threads), (size_t)kSmem, stream, 1u, L);
+  return launch_kernel(gemm_dmma_kernel<kBM, kBN>, dim3(grid), dim3(K1Cfg<kBM, kBN>::kThreads),
+                       (size_t)K1Cfg<kBM, kBN>::kSmem, stream, 1u, L);
+}
+
+// Latency path for small single-descriptor updates (K3's trailing updates):
+// 64 x 64 tiles, one CTA per tile.  Same summation order as launch_gemm.
+cudaError_t launch_gemm_small(const GemmDesc& h, cudaStream_t stream) {
+  cudaError_t e = gemm_init_attributes();
+  if (e != cudaSuccess) return e;
+  if (h.M <= 0 || h.N <= 0 || h.batch <= 0) return cudaSuccess;
+  GemmLaunch L{};
+  L.count = 1;
+  L.inl[0] = h;
+  L.inl[0].tiles_m = (h.M + 63) / 64;
+  L.inl[0].tiles_n = (h.N + 63) / 64;
+  L.inl[0].tile_begin = 0;
+  L.descs = nullptr;
+  L.total_tiles = L.inl[0].tiles_m * L.inl[0].tiles_n * h.batch;
+  return launch_kernel(gemm_dmma_kernel<64, 64>, dim3(L.total_tiles), dim3(K1Cfg<64, 64>::kThreads),
+                       (size_t)K1Cfg<64, 64>::kSmem, stream, 1u, L);
 }
 
 }  // namespace bi

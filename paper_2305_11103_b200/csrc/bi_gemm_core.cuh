@@ -61,11 +61,13 @@ __device__ __forceinline__ void k1_dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// One k-tile of DMMA on a stage (warp tile 32 x 32 at (wm, wn)).
+// One k-tile of DMMA on a stage (warp tile 32 x 32 at (wm, wn)).  StageA is
+// the byte size of the stage's A part (tile rows x 128 B); B follows it.
+template <int StageA = kK1StageA>
 __device__ __forceinline__ void k1_compute(const uint8_t* stage, const K1Frag& f, int wm, int wn, int fr,
                                            double (&acc)[4][4][2]) {
   const uint8_t* sa = stage + (wm * 32 + fr) * 128;
-  const uint8_t* sb = stage + kK1StageA + (wn * 2) * kK1BoxB;
+  const uint8_t* sb = stage + StageA + (wn * 2) * kK1BoxB;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     double af[4], bf[4];
@@ -81,7 +83,11 @@ __device__ __forceinline__ void k1_compute(const uint8_t* stage, const K1Frag& f
 }
 
 // D = [C] + sign * acc with the output column remap; all C loads before any
-// D store (C may alias D).
+// D store (C may alias D).  Every C load of the thread is issued before the
+// first use, so the 16 loads overlap instead of paying one L2/DRAM latency
+// each; full tiles with 16-byte-aligned, even-strided C/D and an even skip
+// window (column pairs never straddle it) take branch-free 16-byte accesses.
+template <int TM = kBM, int TN = kBN>
 __device__ __forceinline__ void k1_epilogue(const GemmDesc& d, int bz, int m0, int n0, int wm, int wn, int fr, int fc,
                                             double (&acc)[4][4][2]) {
   const int mrem = d.M - m0, nrem = d.N - n0;
@@ -90,6 +96,7 @@ __device__ __forceinline__ void k1_epilogue(const GemmDesc& d, int bz, int m0, i
   const double sgn = d.neg ? -1.0 : 1.0;
   const int skip_at = d.skip_at, skip_len = d.skip_len;
   auto pcol = [&](int g) { return g < skip_at ? g : g + skip_len; };
+  const bool full = mrem >= TM && nrem >= TN && ((skip_at | skip_len) & 1) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -98,26 +105,45 @@ __device__ __forceinline__ void k1_epilogue(const GemmDesc& d, int bz, int m0, i
       acc[i][j][1] *= sgn;
     }
   if (C) {
+    const bool vec = full && ((d.ldc & 1) == 0) && ((((uintptr_t)C) & 15) == 0);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = wm * 32 + i * 8 + fr;
-      const int64_t row = m0 + r;
+    for (int h = 0; h < 2; ++h) {  // two rounds of 8 loads in flight (register budget)
+      double2 cv[2][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int cl = wn * 32 + j * 8 + 2 * fc;
-        if (r >= mrem || cl >= nrem) continue;
-        const int p0 = pcol(n0 + cl), p1 = pcol(n0 + cl + 1);
-        const double* cp = C + row * d.ldc + p0;
-        if (cl + 1 < nrem && p1 == p0 + 1 && (((uintptr_t)cp) & 15) == 0) {
-          const double2 cv = __ldg(reinterpret_cast<const double2*>(cp));
-          acc[i][j][0] += cv.x;
-          acc[i][j][1] += cv.y;
-        } else {
-          acc[i][j][0] += cp[0];
-          if (cl + 1 < nrem) acc[i][j][1] += C[row * d.ldc + p1];
+      for (int ii = 0; ii < 2; ++ii) {
+        const int r = wm * 32 + (2 * h + ii) * 8 + fr;
+        const int64_t row = m0 + r;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int cl = wn * 32 + j * 8 + 2 * fc;
+          if (vec) {
+            cv[ii][j] = __ldg(reinterpret_cast<const double2*>(C + row * d.ldc + pcol(n0 + cl)));
+          } else {
+            cv[ii][j] = make_double2(0.0, 0.0);
+            if (r < mrem && cl < nrem) cv[ii][j].x = __ldg(C + row * d.ldc + pcol(n0 + cl));
+            if (r < mrem && cl + 1 < nrem) cv[ii][j].y = __ldg(C + row * d.ldc + pcol(n0 + cl + 1));
+          }
         }
       }
+#pragma unroll
+      for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[2 * h + ii][j][0] += cv[ii][j].x;
+          acc[2 * h + ii][j][1] += cv[ii][j].y;
+        }
     }
+  }
+  if (full && ((d.ldd & 1) == 0) && ((((uintptr_t)D) & 15) == 0)) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = m0 + wm * 32 + i * 8 + fr;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<double2*>(D + row * d.ldd + pcol(n0 + wn * 32 + j * 8 + 2 * fc)) =
+            make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+    return;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -144,6 +170,7 @@ struct K1Tile {
   int desc, bz, m0, n0;
 };
 
+template <int TM = kBM, int TN = kBN>
 __device__ __forceinline__ K1Tile k1_locate(const GemmDesc* table, int count, int tile) {
   int lo = 0, hi = count - 1;
   while (lo < hi) {
@@ -156,7 +183,7 @@ __device__ __forceinline__ K1Tile k1_locate(const GemmDesc* table, int count, in
   const int bz = local / per;
   const int rem = local - bz * per;
   const int tm = rem / d.tiles_n;
-  return K1Tile{lo, bz, tm * kBM, (rem - tm * d.tiles_n) * kBN};
+  return K1Tile{lo, bz, tm * TM, (rem - tm * d.tiles_n) * TN};
 }
 
 }  // namespace bi

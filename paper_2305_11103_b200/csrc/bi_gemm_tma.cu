@@ -153,6 +153,7 @@ cudaError_t tma_init() {
     }
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel);
   });
   return g_tma_err;
 }

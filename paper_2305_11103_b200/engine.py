@@ -302,10 +302,10 @@ class DeviceEngine:
 
     def counters(self, first: int = 1, last: int | None = None) -> dict:
         last = self.n_steps if last is None else last
-        out = (_lib.ctypes.c_double * 5)()
+        out = (_lib.ctypes.c_double * 6)()
         _lib.check(_lib.lib().bi_engine_counters(self._h, first, last, out), "bi_engine_counters")
         return {"multiplies": int(out[0]), "inversions": int(out[1]), "reductions": int(out[2]),
-                "gemm_flops": out[3], "leaf_flops": out[4]}
+                "gemm_flops": out[3], "leaf_flops": out[4], "gemm_bytes": out[5]}
 
     def tset_square(self, level: int, quad: int, matrix: int = 0):
         """Device view of the level-`level` provisional square of a quad."""

@@ -71,7 +71,7 @@ def test_host_abi_validation_without_device(bi):
     sizes = (bi._lib._c_i64 * 4)(4, 4, 4, 4)
     assert lib.bi_engine_create(bi._lib.ctypes.byref(h), 4, sizes, 2) == 0
     assert lib.bi_engine_workspace_bytes(h) > 0
-    out = (bi._lib.ctypes.c_double * 5)()
+    out = (bi._lib.ctypes.c_double * 6)()
     assert lib.bi_engine_counters(h, 1, 7, out) == 0
     assert (out[0], out[1], out[2]) == (20.0, 16.0, 10.0)  # same tallies as the reference engine
     assert lib.bi_engine_destroy(h) == 0
@@ -90,7 +90,7 @@ def test_engine_counters_match_reference_golden(bi):
         h = bi._lib._vp()
         arr = (bi._lib._c_i64 * len(sizes))(*sizes)
         assert lib.bi_engine_create(bi._lib.ctypes.byref(h), len(sizes), arr, 1) == 0
-        out = (bi._lib.ctypes.c_double * 5)()
+        out = (bi._lib.ctypes.c_double * 6)()
         assert lib.bi_engine_counters(h, 1, 2 * len(sizes) - 1, out) == 0
         lib.bi_engine_destroy(h)
         assert [int(out[0]), int(out[1]), int(out[2])] == list(GOLDEN[f"engine_{name}_counters"]), name

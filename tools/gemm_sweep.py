@@ -21,6 +21,9 @@ SHAPES = [  # (m, n, k, batch, accumulate)
     (512, 96, 32, 32, True),   # K3 inner update
     (512, 384, 128, 32, True),  # K3 outer update
     (256, 256, 256, 64, False),
+    (512, 96, 32, 8, True),    # K3 inner update, 8 leaves
+    (512, 384, 128, 8, True),  # K3 outer update, 8 leaves
+    (128, 128, 16, 1, False),  # one tile, one k-tile: launch + pipeline latency
 ]
 
 
@@ -36,7 +39,7 @@ def run_k1(a, b, c, d, batch, neg=False):
     assert rc == 0, L.bi_last_error()
 
 
-def timeit(fn, reps=10):
+def timeit(fn, reps=20):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -69,8 +72,8 @@ def main():
         ref = (c if accum else 0) + torch.bmm(a, b)
         err = (d - ref).norm() / ref.norm()
         t2 = timeit(lambda: torch.baddbmm(c, a, b) if accum else torch.bmm(a, b))
-        print(f"{m}x{n}x{k} b{batch} acc={accum}: K1 {flops / t1 / 1e9:6.2f} TF/s ({t1:.3f} ms)  "
-              f"cuBLAS {flops / t2 / 1e9:6.2f} TF/s ({t2:.3f} ms)  relerr {err:.1e}", flush=True)
+        print(f"{m}x{n}x{k} b{batch} acc={accum}: K1 {flops / t1 / 1e9:6.2f} TF/s ({t1 * 1e3:8.1f} us)  "
+              f"cuBLAS {flops / t2 / 1e9:6.2f} TF/s ({t2 * 1e3:8.1f} us)  relerr {err:.1e}", flush=True)
 
 
 if __name__ == "__main__":
