@@ -192,7 +192,7 @@ struct bi_engine {
   cudaStream_t aux_stream[kMaxLanes] = {};  // lanes 1.. (lane 0 runs on the caller's stream)
   cudaEvent_t ev_fork = nullptr, ev_skew[kMaxLanes] = {}, ev_join[kMaxLanes] = {};
   cudaStream_t copy_stream = nullptr;       // host->device input copies
-  std::vector<cudaEvent_t> ev_h2d;          // one per matrix
+  std::vector<cudaEvent_t> ev_h2d;          // per (matrix, level): that level's input blocks copied
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int last_first = 1, last_last = 0;
 
@@ -486,8 +486,8 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   }
   if (!e->copy_stream) {
     BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
-    e->ev_h2d.assign(e->Z, nullptr);
-    for (int z = 0; z < e->Z; ++z) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_h2d[z], cudaEventDisableTiming));
+    e->ev_h2d.assign((size_t)e->Z * (e->k + 1), nullptr);
+    for (auto& ev : e->ev_h2d) BI_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   if (!e->ev_fork) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
   if (e->nlanes > 1 && !e->ev_skew[0]) {
@@ -563,11 +563,21 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
 }
 
 static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cudaStream_t s, int mask,
-                                cudaEvent_t after_first = nullptr) {
+                                cudaEvent_t after_first = nullptr, bool wait_input = false) {
   // Lane priority: lane 0 highest.  The leading lane then runs as if alone
   // and the others fill the SMs its latency-bound leaf phases leave idle.
   PriorityScope lane_prio(e->lane_priority[lane]);
   for (int stepid = first; stepid <= last; ++stepid) {
+    if (wait_input && (stepid & (stepid - 1)) == 0) {
+      // step 2^l is the first to read M at level l (diag blocks for l = 0,
+      // the level-l quads' off-diagonal blocks for l >= 1)
+      int lv = 0;
+      while ((1 << lv) < stepid) ++lv;
+      for (int z = e->zlo[lane]; z < e->zhi[lane]; ++z) {
+        cudaError_t err = cudaStreamWaitEvent(s, e->ev_h2d[(size_t)z * (e->k + 1) + lv], 0);
+        if (err != cudaSuccess) return err;
+      }
+    }
     for (const Op& op : e->lane_ops[lane][stepid]) {
       if (!(mask & (op.kind == 0 ? 2 : 1))) continue;
       cudaError_t err;
@@ -601,8 +611,7 @@ struct HostIO {
 static cudaError_t lane_io_pre(bi_engine* e, int lane, cudaStream_t ls, int first, const HostIO* io) {
   cudaError_t err = cudaSuccess;
   for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z) {
-    if (io && io->in) err = cudaStreamWaitEvent(ls, e->ev_h2d[z], 0);
-    if (err == cudaSuccess && io && first == 1)
+    if (io && first == 1)
       err = cudaMemset2DAsync(e->Minv + (int64_t)z * e->si, e->ldi * 8, 0, e->n * 8, e->n, ls);
   }
   return err;
@@ -623,12 +632,45 @@ static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t
   const bool fork = e->nlanes > 1 || (io && io->in);
   if (fork) err = cudaEventRecord(e->ev_fork, s);
   if (io && io->in && err == cudaSuccess) {
+    // Input in level order across the batch: every matrix's diagonal blocks
+    // (all step 1 reads), then level by level the quads' off-diagonal B and
+    // C blocks (first read by step 2^l).  Lanes start after a few MB instead
+    // of after their whole matrix, and the rest streams under the compute.
     err = cudaStreamWaitEvent(e->copy_stream, e->ev_fork, 0);
-    for (int z = 0; z < e->Z && err == cudaSuccess; ++z) {
-      err = cudaMemcpy2DAsync(const_cast<double*>(e->M) + (int64_t)z * e->sm, e->ldm * 8,
-                              io->in + (int64_t)z * io->s_in, io->ld_in * 8, e->n * 8, e->n,
-                              cudaMemcpyHostToDevice, e->copy_stream);
-      if (err == cudaSuccess) err = cudaEventRecord(e->ev_h2d[z], e->copy_stream);
+    auto copy_block = [&](int z, int r0, int r1, int c0, int c1) {
+      const int64_t ro = e->off[r0], co = e->off[c0];
+      return cudaMemcpy2DAsync(const_cast<double*>(e->M) + (int64_t)z * e->sm + ro * e->ldm + co, e->ldm * 8,
+                               io->in + (int64_t)z * io->s_in + ro * io->ld_in + co, io->ld_in * 8,
+                               (e->off[c1] - co) * 8, e->off[r1] - ro, cudaMemcpyHostToDevice, e->copy_stream);
+    };
+    // (matrix, level) pieces in order of the step that first needs them: lane
+    // l starts ~l steps late (skew), and reads level lv at step 2^lv
+    std::vector<std::pair<int, int>> order;  // (z, lv)
+    for (int lv = 0; lv <= e->k; ++lv)
+      for (int z = 0; z < e->Z; ++z) order.push_back({z, lv});
+    auto lane_of = [&](int z) {
+      int l = 0;
+      while (l + 1 < e->nlanes && z >= e->zhi[l]) ++l;
+      return l;
+    };
+    std::stable_sort(order.begin(), order.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+      return lane_of(x.first) + (1 << x.second) < lane_of(y.first) + (1 << y.second);
+    });
+    for (const auto& zl : order) {
+      const int z = zl.first, lv = zl.second;
+      if (err != cudaSuccess) break;
+      {
+        if (lv == 0) {
+          for (int p = 0; p < e->nb && err == cudaSuccess; ++p) err = copy_block(z, p, p + 1, p, p + 1);
+        } else {
+          for (int g = 0; g < (e->nb >> lv) && err == cudaSuccess; ++g) {
+            const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+            err = copy_block(z, first, mid, mid, last);
+            if (err == cudaSuccess) err = copy_block(z, mid, last, first, mid);
+          }
+        }
+        if (err == cudaSuccess) err = cudaEventRecord(e->ev_h2d[(size_t)z * (e->k + 1) + lv], e->copy_stream);
+      }
     }
   }
   // Lanes: lane l runs on its own stream, starting after lane l-1 completes
@@ -641,7 +683,7 @@ static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t
     }
     if (err == cudaSuccess) err = lane_io_pre(e, l, ls, first, io);
     if (err == cudaSuccess)
-      err = enqueue_lane(e, l, first, last, ls, mask, e->nlanes > 1 ? e->ev_skew[l] : nullptr);
+      err = enqueue_lane(e, l, first, last, ls, mask, e->nlanes > 1 ? e->ev_skew[l] : nullptr, io && io->in);
   }
   // read-back after every lane is enqueued (a pageable D2H blocks the host)
   for (int l = 0; l < e->nlanes && err == cudaSuccess; ++l) {
