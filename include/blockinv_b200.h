@@ -98,6 +98,16 @@ int bi_inv_batched(int count, int64_t n,
  * ---------------------------------------------------------------------- */
 typedef struct bi_engine bi_engine;
 int bi_engine_create(bi_engine** out, int nblocks, const int64_t* sizes, int batch);
+/* Schedules.  BI_SCHEDULE_EQ7 is the reference step engine above (default;
+ * step/state parity).  BI_SCHEDULE_PIVOT_A runs the 2n^3
+ * pivot-A recursion of invertor_by_a (recursive.py:83-123) at block
+ * granularity instead -- same partition, same K3 leaves, in place in M_inv
+ * -- as one step (N_s = 1): no stop_after_step states, no T-sets, 2n^3
+ * instead of (3 - 1/N_b) n^3 flops.  Singular leaves report step 1 and the
+ * block index as `quad`. */
+#define BI_SCHEDULE_EQ7 0
+#define BI_SCHEDULE_PIVOT_A 1
+int bi_engine_create_ex(bi_engine** out, int nblocks, const int64_t* sizes, int batch, int schedule);
 int64_t bi_engine_workspace_bytes(const bi_engine* e);
 int bi_engine_bind(bi_engine* e,
                    const double* m, int64_t ldm, int64_t stride_m,

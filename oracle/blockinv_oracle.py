@@ -51,6 +51,8 @@ __all__ = [
     "residual_frob",
     "rel_frob",
     "flops_engine",
+    "pivot_a_blocks",
+    "flops_pivot_a",
 ]
 
 
@@ -810,6 +812,64 @@ def run_inversion(m, sizes=None, stop_after_step=None, counts=None, leaf_inverte
     if return_state:
         return minv, tsets
     return minv
+
+
+def pivot_a_blocks(m, sizes, leaf_inverter=None) -> np.ndarray:
+    """The pivot-A recursion of invertor_by_a (recursive.py:83-123, same six
+    products per node, same ascending-k multiply) split at diagonal-block
+    boundaries instead of n//2, with the partition's blocks as leaves -- the
+    device's BI_SCHEDULE_PIVOT_A.  Leaves use
+    ``leaf_inverter`` (default: the pivoted gauss_jordan oracle)."""
+    m = np.asarray(m, dtype=np.float64)
+    sizes = list(sizes)
+    off = offsets_of(sizes)
+    inv_leaf = leaf_inverter or gauss_jordan
+
+    def node(x, b0, b1, path):
+        if b1 - b0 == 1:
+            return inv_leaf(x)  # raises the leaf inverter's singular error
+        mid = (b0 + b1) // 2
+        p = off[mid] - off[b0]
+        q = off[b1] - off[mid]
+        a, b, c, d = x[:p, :p], x[:p, p:], x[p:, :p], x[p:, p:]
+        ainv = node(a, b0, mid, path + ["A"])
+        n_ab = np.empty((p, q))
+        multiply(ainv, b, n_ab, negate=True)
+        ca = np.empty((q, p))
+        multiply(c, ainv, ca)
+        s_a = d.copy()
+        multiply(c, n_ab, s_a, accumulate=True)
+        sinv = node(s_a, mid, b1, path + ["SchurA"])
+        out = np.empty((p + q, p + q))
+        multiply(n_ab, sinv, out[:p, p:])
+        out[:p, :p] = ainv
+        multiply(out[:p, p:], ca, out[:p, :p], accumulate=True, negate=True)
+        multiply(sinv, ca, out[p:, :p], negate=True)
+        out[p:, p:] = sinv
+        return out
+
+    return node(m, 0, len(sizes), [])
+
+
+def flops_pivot_a(sizes) -> dict:
+    """Flops of pivot_a_blocks: 6pq(p+q) per node, 2b^3 per leaf (= 2n^3 for
+    equal power-of-two partitions)."""
+    sizes = list(sizes)
+    off = offsets_of(sizes)
+    out = {"leaves": sum(2.0 * s**3 for s in sizes), "nodes": 0.0}
+
+    def node(b0, b1):
+        if b1 - b0 == 1:
+            return
+        mid = (b0 + b1) // 2
+        p, q = off[mid] - off[b0], off[b1] - off[mid]
+        out["nodes"] += 6.0 * p * q * (p + q)
+        node(b0, mid)
+        node(mid, b1)
+
+    node(0, len(sizes))
+    out["total"] = out["leaves"] + out["nodes"]
+    return out
 
 
 def flops_engine(sizes) -> dict:

@@ -20,6 +20,7 @@
 //  * singular leaves are recorded per diag step on the device and resolved
 //    to (step, quad, matrix) after the range (no host syncs inside it).
 #include <algorithm>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -116,8 +117,8 @@ using namespace bi;
 namespace {
 
 struct Op {
-  int kind;      // 0 = inversion group, 1 = gemm launch
-  int index;     // inv group index / gemm launch index
+  int kind;      // 0 = inversion group, 1 = gemm launch, 2 = copy M -> M_inv (pivot-A)
+  int index;     // inv group index / gemm launch index / lane
 };
 
 struct GemmLaunchRec {
@@ -131,6 +132,7 @@ struct InvRec {
   std::vector<int> item_matrix;  // matrix index z of each item
   int info_offset;      // into the info region (ints)
   int lane;             // which lane (scratch region / stream)
+  bool in_place = false;  // pivot-A: leaf inverted in place inside M_inv
 };
 
 struct Window {
@@ -153,6 +155,8 @@ struct GraphKey {
 
 struct bi_engine {
   int nb = 0, Z = 0, k = 0, nsteps = 0;
+  int schedule = 0;                  // BI_SCHEDULE_EQ7 / BI_SCHEDULE_PIVOT_A
+  std::vector<int64_t> pa_depth_off;  // pivot-A: per recursion depth, T_b/T_c offset (elements)
   std::vector<int64_t> sizes, off;
   int64_t n = 0;
   // bound buffers
@@ -237,7 +241,25 @@ struct bi_engine {
 static int64_t align256(int64_t v) { return round_up(v, 256); }
 
 extern "C" int bi_engine_create(bi_engine** out, int nblocks, const int64_t* sizes, int batch) {
+  return bi_engine_create_ex(out, nblocks, sizes, batch, BI_SCHEDULE_EQ7);
+}
+
+// pivot-A recursion tree over blocks [b0, b1): per depth, the largest T_b
+// (p x ld(q)) + T_c (q x ld(p)) footprint of its nodes
+static void pivot_a_footprint(const std::vector<int64_t>& off, int b0, int b1, int depth,
+                              std::vector<int64_t>& per_depth) {
+  if (b1 - b0 < 2) return;
+  const int mid = (b0 + b1) / 2;
+  const int64_t p = off[mid] - off[b0], q = off[b1] - off[mid];
+  if ((int)per_depth.size() <= depth) per_depth.resize(depth + 1, 0);
+  per_depth[depth] = std::max(per_depth[depth], round_up(p * round_up(q, 4), 32) + round_up(q * round_up(p, 4), 32));
+  pivot_a_footprint(off, b0, mid, depth + 1, per_depth);
+  pivot_a_footprint(off, mid, b1, depth + 1, per_depth);
+}
+
+extern "C" int bi_engine_create_ex(bi_engine** out, int nblocks, const int64_t* sizes, int batch, int schedule) {
   BI_REQUIRE(out != nullptr && sizes != nullptr, "null argument");
+  BI_REQUIRE(schedule == BI_SCHEDULE_EQ7 || schedule == BI_SCHEDULE_PIVOT_A, "unknown schedule");
   BI_REQUIRE(nblocks >= 1 && (nblocks & (nblocks - 1)) == 0,
              "number of diagonal blocks must be a power of two");
   BI_REQUIRE(batch >= 1, "batch must be >= 1");
@@ -245,7 +267,8 @@ extern "C" int bi_engine_create(bi_engine** out, int nblocks, const int64_t* siz
   e->nb = nblocks;
   e->Z = batch;
   while ((1 << e->k) < nblocks) ++e->k;
-  e->nsteps = 2 * nblocks - 1;
+  e->schedule = schedule;
+  e->nsteps = schedule == BI_SCHEDULE_PIVOT_A ? 1 : 2 * nblocks - 1;
   e->off.push_back(0);
   int64_t maxb = 0;
   for (int i = 0; i < nblocks; ++i) {
@@ -268,6 +291,16 @@ extern "C" int bi_engine_create(bi_engine** out, int nblocks, const int64_t* siz
       t += round_up(side * ld, 32);
     }
   }
+  if (schedule == BI_SCHEDULE_PIVOT_A) {  // no T-sets: per-depth T_b / T_c temporaries instead
+    std::vector<int64_t> per_depth;
+    pivot_a_footprint(e->off, 0, nblocks, 0, per_depth);
+    t = 0;
+    e->pa_depth_off.clear();
+    for (int64_t f : per_depth) {
+      e->pa_depth_off.push_back(t);
+      t += f;
+    }
+  }
   e->t_matrix = t;
   e->t_bytes = align256(t * 8 * (int64_t)batch);
   // Lanes: with >= 2 matrices the batch is split in two halves that run on two
@@ -285,11 +318,15 @@ extern "C" int bi_engine_create(bi_engine** out, int nblocks, const int64_t* siz
   std::map<int64_t, int> cnt;
   int lane_max = 0;
   for (int l = 0; l < e->nlanes; ++l) lane_max = std::max(lane_max, e->zhi[l] - e->zlo[l]);
-  for (int64_t s : e->sizes) cnt[s] += lane_max;
+  for (int64_t s : e->sizes) {
+    if (schedule == BI_SCHEDULE_PIVOT_A) cnt[s] = lane_max;  // one leaf at a time per lane
+    else cnt[s] += lane_max;
+  }
   int64_t scratch = 0;
   for (auto& kv : cnt) scratch = std::max(scratch, inv_group_scratch_bytes((int)kv.first, kv.second));
   e->inv_scratch = align256(scratch);
-  e->info_ints = (int64_t)nblocks * nblocks * batch;  // nblocks diag steps x leaves
+  // Eq. 7: nblocks diag steps x leaves; pivot-A: every block is a leaf once
+  e->info_ints = (int64_t)(schedule == BI_SCHEDULE_PIVOT_A ? 1 : nblocks) * nblocks * batch;
   // metadata upper bound (descriptors + pointer tables); computed exactly at bind
   *out = e.release();
   return 0;
@@ -301,7 +338,10 @@ extern "C" int64_t bi_engine_workspace_bytes(const bi_engine* e) {
   return e->t_bytes + e->nlanes * e->inv_scratch + align256(e->info_ints * 4);
 }
 
+static int build_pivot_a(bi_engine* e);
+
 static int build_schedule(bi_engine* e) {
+  if (e->schedule == BI_SCHEDULE_PIVOT_A) return build_pivot_a(e);
   for (int l = 0; l < bi_engine::kMaxLanes; ++l) e->lane_ops[l].assign(e->nsteps + 1, {});
   e->descs.clear();
   e->launches.clear();
@@ -438,6 +478,106 @@ static int build_schedule(bi_engine* e) {
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// pivot-A schedule: the 2n^3 recursion of invertor_by_a
+// (recursive.py:83-123) at block granularity, in place in M_inv, batched over
+// the lane's matrices.  Node over blocks [b0, b1) split at mid (p, q rows):
+//   recurse on A                          -> A = A^-1
+//   T_b = -A B,  T_c = -C A               (one launch)
+//   D  += C T_b                           (S_A = D - C A^-1 B)
+//   recurse on D                          -> D = S_A^-1
+//   C   = D T_c,  B = T_b D               (one launch: -S^-1 C A^-1, -A^-1 B S^-1)
+//   A  += T_b C                           (A^-1 + A^-1 B S^-1 C A^-1)
+// 12 p q (p + q) / 2 ... = 6pq(p+q) flops per node, 2n^3 in total with the
+// leaves; T_b / T_c live in per-depth workspace regions.
+// ---------------------------------------------------------------------------
+static int build_pivot_a(bi_engine* e) {
+  for (int l = 0; l < bi_engine::kMaxLanes; ++l) e->lane_ops[l].assign(e->nsteps + 1, {});
+  e->descs.clear();
+  e->launches.clear();
+  e->invs.clear();
+  e->diag_steps.assign(1, 1);
+  const auto& off = e->off;
+  auto add_launch = [&](const std::vector<GemmDesc>& raw) -> int {
+    std::vector<GemmDesc> m = merge_descs(raw);
+    GemmLaunchRec rec{(int)e->descs.size(), (int)m.size()};
+    finalize_descs(m.data(), (int)m.size());
+    e->descs.insert(e->descs.end(), m.begin(), m.end());
+    e->launches.push_back(rec);
+    return (int)e->launches.size() - 1;
+  };
+  auto gemm = [](const double* a, int64_t lda, const double* b, int64_t ldb, const double* c, int64_t ldc,
+                 double* d, int64_t ldd, int64_t M, int64_t N, int64_t K, int neg) {
+    GemmDesc g{};
+    g.A = a;
+    g.lda = lda;
+    g.B = b;
+    g.ldb = ldb;
+    g.C = c;
+    g.ldc = c ? ldc : 0;
+    g.D = d;
+    g.ldd = ldd;
+    g.M = (int)M;
+    g.N = (int)N;
+    g.K = (int)K;
+    g.batch = 1;
+    g.neg = neg;
+    g.skip_at = INT32_MAX;
+    g.skip_len = 0;
+    return g;
+  };
+  int info_cursor = 0;
+  for (int lane = 0; lane < e->nlanes; ++lane) {
+    const int Z0 = e->zlo[lane], Z1 = e->zhi[lane];
+    auto& ops = e->lane_ops[lane][1];
+    ops.push_back({2, lane});
+    auto mi = [&](int z, int br, int bc) { return e->Minv + (int64_t)z * e->si + off[br] * e->ldi + off[bc]; };
+    std::function<void(int, int, int)> node = [&](int b0, int b1, int depth) {
+      if (b1 - b0 == 1) {
+        InvRec r{};
+        r.g.n = (int)e->sizes[b0];
+        r.g.count = Z1 - Z0;
+        r.diag_step_index = 0;
+        r.lane = lane;
+        r.info_offset = info_cursor;
+        r.in_place = true;
+        info_cursor += r.g.count;
+        for (int z = Z0; z < Z1; ++z) {
+          r.item_matrix.push_back(z);
+          r.item_block.push_back(b0);
+        }
+        e->invs.push_back(std::move(r));
+        ops.push_back({0, (int)e->invs.size() - 1});
+        return;
+      }
+      const int mid = (b0 + b1) / 2;
+      const int64_t p = off[mid] - off[b0], q = off[b1] - off[mid];
+      const int64_t ldb_t = round_up(q, 4), ldc_t = round_up(p, 4);
+      const int64_t ld = e->ldi;
+      auto tb = [&](int z) { return e->T + (int64_t)z * e->t_matrix + e->pa_depth_off[depth]; };
+      auto tc = [&](int z) { return tb(z) + round_up(p * ldb_t, 32); };
+      node(b0, mid, depth + 1);
+      std::vector<GemmDesc> l1, l2, l3, l4;
+      for (int z = Z0; z < Z1; ++z) {
+        double *A = mi(z, b0, b0), *B = mi(z, b0, mid), *C = mi(z, mid, b0), *D = mi(z, mid, mid);
+        l1.push_back(gemm(A, ld, B, ld, nullptr, 0, tb(z), ldb_t, p, q, p, 1));   // T_b = -A^-1 B
+        l1.push_back(gemm(C, ld, A, ld, nullptr, 0, tc(z), ldc_t, q, p, p, 1));   // T_c = -C A^-1
+        l2.push_back(gemm(C, ld, tb(z), ldb_t, D, ld, D, ld, q, q, p, 0));        // S_A = D + C T_b
+        l3.push_back(gemm(D, ld, tc(z), ldc_t, nullptr, 0, C, ld, q, p, q, 0));   // C = S^-1 T_c
+        l3.push_back(gemm(tb(z), ldb_t, D, ld, nullptr, 0, B, ld, p, q, q, 0));   // B = T_b S^-1
+        l4.push_back(gemm(tb(z), ldb_t, C, ld, A, ld, A, ld, p, p, q, 0));        // A += T_b C
+      }
+      ops.push_back({1, add_launch(l1)});
+      ops.push_back({1, add_launch(l2)});
+      node(mid, b1, depth + 1);
+      ops.push_back({1, add_launch(l3)});
+      ops.push_back({1, add_launch(l4)});
+    };
+    node(0, e->nb, 0);
+  }
+  return 0;
+}
+
 extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_t stride_m, double* minv,
                               int64_t ldi, int64_t stride_i, void* workspace, int64_t workspace_bytes,
                               void* stream) {
@@ -540,7 +680,7 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
     auto* dstld = reinterpret_cast<int64_t*>(host_meta.data() + tabs[i].dstld);
     for (int it = 0; it < r.g.count; ++it) {
       const int z = r.item_matrix[it], pb = r.item_block[it];
-      Window s = e->source(a, z, pb, pb + 1, pb, pb + 1);
+      Window s = r.in_place ? e->minv_window(z, pb, pb) : e->source(a, z, pb, pb + 1, pb, pb + 1);
       Window d = e->minv_window(z, pb, pb);
       src[it] = s.p;
       srcld[it] = s.ld;
@@ -569,19 +709,27 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
   PriorityScope lane_prio(e->lane_priority[lane]);
   for (int stepid = first; stepid <= last; ++stepid) {
     if (wait_input && (stepid & (stepid - 1)) == 0) {
-      // step 2^l is the first to read M at level l (diag blocks for l = 0,
-      // the level-l quads' off-diagonal blocks for l >= 1)
+      // Eq. 7: step 2^l is the first to read M at level l (diag blocks for
+      // l = 0, the level-l quads' off-diagonal blocks for l >= 1).  pivot-A
+      // copies the whole input into M_inv first: wait for every level.
       int lv = 0;
       while ((1 << lv) < stepid) ++lv;
-      for (int z = e->zlo[lane]; z < e->zhi[lane]; ++z) {
-        cudaError_t err = cudaStreamWaitEvent(s, e->ev_h2d[(size_t)z * (e->k + 1) + lv], 0);
-        if (err != cudaSuccess) return err;
-      }
+      const int lv_hi = e->schedule == BI_SCHEDULE_PIVOT_A ? e->k : lv;
+      for (int z = e->zlo[lane]; z < e->zhi[lane]; ++z)
+        for (int l = (e->schedule == BI_SCHEDULE_PIVOT_A ? 0 : lv); l <= lv_hi; ++l) {
+          cudaError_t err = cudaStreamWaitEvent(s, e->ev_h2d[(size_t)z * (e->k + 1) + l], 0);
+          if (err != cudaSuccess) return err;
+        }
     }
     for (const Op& op : e->lane_ops[lane][stepid]) {
       if (!(mask & (op.kind == 0 ? 2 : 1))) continue;
       cudaError_t err;
-      if (op.kind == 0) {
+      if (op.kind == 2) {  // pivot-A: the lane's inputs into M_inv (inverted in place)
+        err = cudaSuccess;
+        for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z)
+          err = cudaMemcpy2DAsync(e->Minv + (int64_t)z * e->si, e->ldi * 8, e->M + (int64_t)z * e->sm, e->ldm * 8,
+                                  e->n * 8, e->n, cudaMemcpyDeviceToDevice, s);
+      } else if (op.kind == 0) {
         PriorityScope leaf_prio(e->leaf_priority ? e->leaf_priority : g_launch_priority);
         err = launch_inv_group(e->invs[op.index].g, s);
       } else {
@@ -611,7 +759,7 @@ struct HostIO {
 static cudaError_t lane_io_pre(bi_engine* e, int lane, cudaStream_t ls, int first, const HostIO* io) {
   cudaError_t err = cudaSuccess;
   for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z) {
-    if (io && first == 1)
+    if (io && first == 1 && e->schedule == BI_SCHEDULE_EQ7)
       err = cudaMemset2DAsync(e->Minv + (int64_t)z * e->si, e->ldi * 8, 0, e->n * 8, e->n, ls);
   }
   return err;
@@ -780,6 +928,7 @@ extern "C" int bi_engine_launches(const bi_engine* e, int first_step, int last_s
   for (int lane = 0; lane < e->nlanes; ++lane)
   for (int stepid = first_step; stepid <= last_step; ++stepid)
     for (const Op& op : e->lane_ops[lane][stepid]) {
+      if (op.kind == 2) continue;  // copy, not a kernel
       if (op.kind == 1) {
         gemm += 1;
       } else {
@@ -836,7 +985,27 @@ extern "C" int bi_engine_counters(const bi_engine* e, int first_step, int last_s
   BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps, "stepid outside 1..N_s");
   double mult = 0, invs = 0, red = 0, gflops = 0, lflops = 0, gbytes = 0;
   const auto& off = e->off;
-  for (int stepid = first_step; stepid <= last_step; ++stepid) {
+  if (e->schedule == BI_SCHEDULE_PIVOT_A) {  // invertor_by_a tallies: 6 multiplies (2 accumulating) per node
+    std::function<void(int, int)> node = [&](int b0, int b1) {
+      if (b1 - b0 == 1) {
+        invs += 1;
+        lflops += 2.0 * (double)e->sizes[b0] * e->sizes[b0] * e->sizes[b0];
+        return;
+      }
+      const int mid = (b0 + b1) / 2;
+      const double p = (double)(off[mid] - off[b0]), q = (double)(off[b1] - off[mid]);
+      mult += 6;
+      red += 2;
+      gflops += 6.0 * p * q * (p + q);
+      // T_b, T_c: read A and B / C, write; D += C T_b; C = D T_c; B = T_b D; A += T_b C
+      gbytes += 8.0 * ((p * p + 2 * p * q) + (p * p + 2 * p * q) + (2 * p * q + 2 * q * q) +
+                       (q * q + 2 * p * q) + (q * q + 2 * p * q) + (2 * p * q + 2 * p * p));
+      node(b0, mid);
+      node(mid, b1);
+    };
+    node(0, e->nb);
+  }
+  for (int stepid = first_step; stepid <= last_step && e->schedule == BI_SCHEDULE_EQ7; ++stepid) {
     StepAct a;
     loopid_decode(stepid, e->nb, &a);
     if (a.kind == 0 || a.kind == 2) {
@@ -879,6 +1048,7 @@ extern "C" int bi_engine_counters(const bi_engine* e, int first_step, int last_s
 extern "C" int bi_engine_tset_square(const bi_engine* e, int level, int quad, int matrix, double** ptr,
                                      int64_t* ld, int64_t* side) {
   BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(e->schedule == BI_SCHEDULE_EQ7, "the pivot-A schedule keeps no T-sets");
   BI_REQUIRE(level >= 1 && level <= e->k && quad >= 0 && quad < (e->nb >> level) && matrix >= 0 &&
                  matrix < e->Z,
              "tset index out of range");

@@ -207,6 +207,17 @@ __global__ void __launch_bounds__(K1Cfg<TM, TN>::kThreads) gemm_dmma_kernel(cons
 std::once_flag g_attr_once;
 cudaError_t g_attr_err = cudaSuccess;
 
+int small_tile_threshold() {  // BI_GEMM_SMALL_TILES: 128-tile count below which 64 x 64 tiles are used
+  static const int v = [] {
+    const char* e = getenv("BI_GEMM_SMALL_TILES");
+    if (e) return atoi(e);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }();
+  return v;
+}
+
 int use_tma() {
   static const int v = [] {
     const char* e = getenv("BI_GEMM_TMA");
@@ -242,6 +253,8 @@ cudaError_t gemm_init_attributes() {
   return g_attr_err;
 }
 
+cudaError_t launch_gemm_small_n(const GemmDesc* h, int count, cudaStream_t stream);
+
 cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int count, cudaStream_t stream) {
   if (count <= 0) return cudaSuccess;
   cudaError_t e = gemm_init_attributes();
@@ -250,6 +263,9 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
   const int total =
       last.tile_begin + ((last.M <= 0 || last.N <= 0 || last.batch <= 0) ? 0 : last.tiles_m * last.tiles_n * last.batch);
   if (total == 0) return cudaSuccess;
+  // Launches whose 128-tile grid cannot fill the GPU are latency-bound (one
+  // FP64 SM needs ~4 us per 128 x 128 x 16 k-tile): 64 x 64 tiles, 4x the CTAs.
+  if (count <= kGemmInline && total < small_tile_threshold()) return launch_gemm_small_n(h_descs, count, stream);
   if (use_tma()) {
     cudaError_t te = cudaSuccess;
     if (launch_gemm_tma(h_descs, count, g_gemm_grid_cap, stream, &te)) return te;
@@ -269,22 +285,31 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
                        (size_t)K1Cfg<kBM, kBN>::kSmem, stream, 1u, L);
 }
 
-// Latency path for small single-descriptor updates (K3's trailing updates):
-// 64 x 64 tiles, one CTA per tile.  Same summation order as launch_gemm.
-cudaError_t launch_gemm_small(const GemmDesc& h, cudaStream_t stream) {
+// Latency path: <= kGemmInline descriptors on 64 x 64 tiles, one CTA per tile
+// (4x the CTAs of the 128 x 128 tiling).  Same summation order as launch_gemm.
+cudaError_t launch_gemm_small_n(const GemmDesc* h, int count, cudaStream_t stream) {
   cudaError_t e = gemm_init_attributes();
   if (e != cudaSuccess) return e;
-  if (h.M <= 0 || h.N <= 0 || h.batch <= 0) return cudaSuccess;
+  if (count <= 0 || count > kGemmInline) return cudaErrorInvalidValue;
   GemmLaunch L{};
-  L.count = 1;
-  L.inl[0] = h;
-  L.inl[0].tiles_m = (h.M + 63) / 64;
-  L.inl[0].tiles_n = (h.N + 63) / 64;
-  L.inl[0].tile_begin = 0;
+  L.count = count;
   L.descs = nullptr;
-  L.total_tiles = L.inl[0].tiles_m * L.inl[0].tiles_n * h.batch;
-  return launch_kernel(gemm_dmma_kernel<64, 64>, dim3(L.total_tiles), dim3(K1Cfg<64, 64>::kThreads),
+  int t = 0;
+  for (int i = 0; i < count; ++i) {
+    GemmDesc d = h[i];
+    const bool empty = d.M <= 0 || d.N <= 0 || d.batch <= 0;
+    d.tiles_m = empty ? 0 : (d.M + 63) / 64;
+    d.tiles_n = empty ? 1 : (d.N + 63) / 64;
+    d.tile_begin = t;
+    t += empty ? 0 : d.tiles_m * d.tiles_n * d.batch;
+    L.inl[i] = d;
+  }
+  L.total_tiles = t;
+  if (t == 0) return cudaSuccess;
+  return launch_kernel(gemm_dmma_kernel<64, 64>, dim3(t), dim3(K1Cfg<64, 64>::kThreads),
                        (size_t)K1Cfg<64, 64>::kSmem, stream, 1u, L);
 }
+
+cudaError_t launch_gemm_small(const GemmDesc& h, cudaStream_t stream) { return launch_gemm_small_n(&h, 1, stream); }
 
 }  // namespace bi

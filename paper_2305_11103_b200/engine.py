@@ -189,23 +189,32 @@ def fox_block_multiply(a: BlockedView, b: BlockedView, out: BlockedView, workers
 # ---------------------------------------------------------------------------
 
 
+# Device schedules (include/blockinv_b200.h): "eq7" is the reference step
+# engine (default; step/state parity); "pivot_a" is the 2n^3 block-level
+# invertor_by_a recursion, one step, no stop_after_step.
+SCHEDULES = {"eq7": 0, "pivot_a": 1}
+
+
 class DeviceEngine:
     """A bound native engine (``bi_engine``) for one partition and batch size,
     with its device buffers: M and M_inv as [batch, n, ld] float64 tensors and
     the workspace holding every provisional set and the leaf scratch."""
 
-    def __init__(self, sizes, batch: int = 1):
+    def __init__(self, sizes, batch: int = 1, schedule: str = "eq7"):
         t = _lib.torch()
         _lib.require_device()
+        if schedule not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}, got {schedule!r}")
         self.scheme = partition_from_sizes(sizes)
         self.sizes = tuple(int(s) for s in sizes)
         self.batch = int(batch)
+        self.schedule = schedule
         self.n = self.scheme.m_n
         L = _lib.lib()
         h = _lib._vp()
         arr = (_lib._c_i64 * len(self.sizes))(*self.sizes)
-        _lib.check(L.bi_engine_create(_lib.ctypes.byref(h), len(self.sizes), arr, self.batch),
-                   "bi_engine_create")
+        _lib.check(L.bi_engine_create_ex(_lib.ctypes.byref(h), len(self.sizes), arr, self.batch,
+                                         SCHEDULES[schedule]), "bi_engine_create_ex")
         self._h = h
         self.M = _lib.empty_matrix(self.n, self.n, batch=self.batch)
         self.Minv = _lib.empty_matrix(self.n, self.n, batch=self.batch)
@@ -216,7 +225,7 @@ class DeviceEngine:
                                         _lib.ptr(self.Minv), _lib.ld(self.Minv), int(self.Minv.stride(0)),
                                         _lib.ptr(self.ws), self.ws.numel(), _lib.stream_ptr()),
                        "bi_engine_bind")
-        self.n_steps = total_steps(len(self.sizes))
+        self.n_steps = total_steps(len(self.sizes)) if schedule == "eq7" else 1
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -326,12 +335,13 @@ _ENGINES: "OrderedDict[tuple, DeviceEngine]" = OrderedDict()
 _CACHE_MAX = 2
 
 
-def _engine_for(sizes, batch: int) -> DeviceEngine:
+def _engine_for(sizes, batch: int, schedule: str = "eq7") -> DeviceEngine:
     t = _lib.torch()
-    key = (tuple(int(s) for s in sizes), int(batch), t.cuda.current_device() if t.cuda.is_available() else -1)
+    key = (tuple(int(s) for s in sizes), int(batch), schedule,
+           t.cuda.current_device() if t.cuda.is_available() else -1)
     eng = _ENGINES.get(key)
     if eng is None:
-        eng = DeviceEngine(sizes, batch)
+        eng = DeviceEngine(sizes, batch, schedule)
         _ENGINES[key] = eng
         while len(_ENGINES) > _CACHE_MAX:
             _ENGINES.popitem(last=False)
@@ -361,18 +371,29 @@ def _last_step(n_steps: int, stop_after_step) -> int:
     return max(1, min(int(stop_after_step), n_steps))
 
 
+def _check_schedule(schedule: str, stop_after_step) -> None:
+    if schedule not in SCHEDULES:
+        raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}, got {schedule!r}")
+    if schedule != "eq7" and stop_after_step is not None:
+        raise ValueError("stop_after_step addresses the Eq. 7 step schedule; use schedule='eq7'")
+
+
 def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backed: bool = False,
                   sizes=None, stop_after_step: int | None = None,
-                  counters: OpCounters | None = None) -> BlockMatrix:
+                  counters: OpCounters | None = None, *, schedule: str = "eq7") -> BlockMatrix:
     """Invert a partitioned matrix through the full step schedule on the B200
     (engine.py:482-542).  Same arguments and result type as the reference;
     ``checkpoint_dir`` / ``file_backed`` (disk persistence, SURVEY 8f #3) are
-    not part of the device path and raise NotImplementedError."""
+    not part of the device path and raise NotImplementedError.
+    Extension: ``schedule="pivot_a"`` runs the same partition through the 2n^3
+    block-level pivot-A recursion (invertor_by_a, recursive.py:83-123) instead
+    of the Eq. 7 steps (SURVEY 8f #1); counters then follow invertor_by_a."""
     resolve_workers(workers)
+    _check_schedule(schedule, stop_after_step)
     if checkpoint_dir is not None or file_backed:
         raise NotImplementedError("checkpoint/resume and file-backed stores are not on the B200 path")
     scheme, dense = _scheme_and_dense(m, sizes)
-    eng = _engine_for(scheme.sizes, 1)
+    eng = _engine_for(scheme.sizes, 1, schedule)
     last = _last_step(eng.n_steps, stop_after_step)
     dense = np.ascontiguousarray(dense, dtype=np.float64)
     out = np.empty((scheme.m_n, scheme.m_n))
@@ -388,7 +409,7 @@ def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backe
 
 def run_inversion_batch(ms, sizes, out: np.ndarray | None = None,
                         stop_after_step: int | None = None,
-                        counters: OpCounters | None = None) -> np.ndarray:
+                        counters: OpCounters | None = None, *, schedule: str = "eq7") -> np.ndarray:
     """Batched extension: invert ``ms`` [batch, n, n] (shared partition
     ``sizes``) in lock-step; returns (or fills ``out``) [batch, n, n].
     Page-locked ``ms``/``out`` make the host<->device copies asynchronous DMA."""
@@ -403,7 +424,8 @@ def run_inversion_batch(ms, sizes, out: np.ndarray | None = None,
     scheme = partition_from_sizes(sizes)
     if scheme.m_n != ms_np.shape[1]:
         raise DimensionMismatch(f"sizes sum to {scheme.m_n}, matrix order is {ms_np.shape[1]}")
-    eng = _engine_for(scheme.sizes, int(ms_np.shape[0]))
+    _check_schedule(schedule, stop_after_step)
+    eng = _engine_for(scheme.sizes, int(ms_np.shape[0]), schedule)
     last = _last_step(eng.n_steps, stop_after_step)
     if out is None:
         out = np.empty(ms_np.shape)

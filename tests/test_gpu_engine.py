@@ -276,3 +276,52 @@ def test_cfg3_full_scale_residual(bi):
     res = bi.residual_frobenius(m, out)
     assert res <= 6000 * np.finfo(float).eps * 1.1e7, res
     assert res <= 1e-6, res
+
+
+# --- pivot-A schedule: block-level invertor_by_a recursion ---
+
+@pytest.mark.parametrize("sizes", [[16] * 8, [7, 9, 12, 4], [64] * 8, [37, 64, 1, 90], [256, 256], [33] * 32, [5],
+                                   [128] * 4])
+def test_pivot_a_schedule_vs_oracle(bi, sizes):
+    n = sum(sizes)
+    m = well_conditioned(n, 91 + n)
+    inv = bi.run_inversion(m, sizes=sizes, schedule="pivot_a").to_dense()
+    _assert_ref_criteria(m, inv, oracle.pivot_a_blocks(m, sizes))
+    assert oracle.rel_frob(inv, oracle.gauss_jordan(m)) <= 1e-9
+
+
+def test_pivot_a_batch_lanes_host_io(bi):
+    """Batch of 3 (three lanes), page-locked and pageable host buffers, equal
+    to the single-matrix runs bitwise; the Eq. 7 engine gives the same inverse
+    to 1e-12."""
+    import torch
+
+    sizes = [24] * 8
+    n = sum(sizes)
+    ms = np.stack([well_conditioned(n, 500 + i) for i in range(3)])
+    single = np.stack([bi.run_inversion(ms[i], sizes=sizes, schedule="pivot_a").to_dense() for i in range(3)])
+    got = bi.run_inversion_batch(ms, sizes, schedule="pivot_a")
+    assert np.array_equal(got, single)
+    pin_in = torch.from_numpy(ms).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+    bi.run_inversion_batch(pin_in.numpy(), sizes, out=pin_out.numpy(), schedule="pivot_a")
+    assert np.array_equal(pin_out.numpy(), single)
+    eq7 = bi.run_inversion_batch(ms, sizes)
+    for i in range(3):
+        assert oracle.rel_frob(single[i], eq7[i]) <= 1e-12
+
+
+def test_pivot_a_singular_leaf_and_arguments(bi):
+    sizes = [4] * 4
+    m = well_conditioned(16, 3)
+    m[:4, :4] = 1.0  # rank-1 leading block: the first leaf of the recursion
+    with pytest.raises(bi.SingularBlock) as ei:
+        bi.run_inversion(m, sizes=sizes, schedule="pivot_a")
+    assert ei.value.step == 1 and ei.value.quad == 0
+    with pytest.raises(ValueError):
+        bi.run_inversion(well_conditioned(16, 4), sizes=sizes, schedule="pivot_a", stop_after_step=2)
+    with pytest.raises(ValueError):
+        bi.run_inversion(well_conditioned(16, 4), sizes=sizes, schedule="lu")
+    c = bi.OpCounters()
+    bi.run_inversion(well_conditioned(16, 4), sizes=sizes, schedule="pivot_a", counters=c)
+    assert (c.multiplies, c.inversions, c.reductions) == (18, 4, 6)

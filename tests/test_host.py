@@ -80,6 +80,27 @@ def test_host_abi_validation_without_device(bi):
     assert lib.bi_inv_workspace_bytes(3, 512) > 3 * 512 * 512 * 8
 
 
+@pytest.mark.parametrize("sizes", [[512] * 8, [3, 9, 5, 11], [7]])
+def test_engine_pivot_a_schedule_counters(bi, sizes):
+    """BI_SCHEDULE_PIVOT_A: one step, invertor_by_a tallies (6 multiplies, 2
+    accumulating, per node; every block inverted once) and 2n^3 flops."""
+    lib = bi.load_library()
+    h = bi._lib._vp()
+    arr = (bi._lib._c_i64 * len(sizes))(*sizes)
+    assert lib.bi_engine_create_ex(bi._lib.ctypes.byref(h), len(sizes), arr, 3, 1) == 0
+    assert lib.bi_engine_workspace_bytes(h) > 0
+    out = (bi._lib.ctypes.c_double * 6)()
+    assert lib.bi_engine_counters(h, 1, 1, out) == 0
+    assert lib.bi_engine_counters(h, 1, 2, out) == bi._lib.BI_EDIM  # one step only
+    assert lib.bi_engine_counters(h, 1, 1, out) == 0
+    nb, n = len(sizes), sum(sizes)
+    assert (out[0], out[1], out[2]) == (6.0 * (nb - 1), float(nb), 2.0 * (nb - 1))
+    assert out[3] + out[4] == 3 * 2.0 * n**3  # batch of 3
+    assert out[4] == 3 * sum(2.0 * s**3 for s in sizes)
+    lib.bi_engine_destroy(h)
+    assert lib.bi_engine_create_ex(bi._lib.ctypes.byref(h), len(sizes), arr, 1, 7) == bi._lib.BI_EDIM
+
+
 def test_engine_counters_match_reference_golden(bi):
     """Native counter tallies == reference OpCounters for every golden case."""
     from test_oracle import ENGINE_CASES

@@ -106,6 +106,23 @@ def test_recursive_and_gj_vs_golden(order):
     assert oracle.gauss_jordan(m).tobytes() == GOLDEN[f"gj_{order}"].tobytes()
 
 
+@pytest.mark.parametrize("sizes", [[32] * 2, [16] * 4, [8] * 8])
+def test_pivot_a_blocks_pinned_to_reference_by_a(sizes):
+    """Block-level pivot-A (the device's pivot_a schedule) with invertor_by_a
+    leaves and equal power-of-two blocks splits exactly where the reference's
+    invertor_by_a does (recursive.py:83-123): bitwise equal to the golden
+    generated from the reference."""
+    m = well_conditioned(64, 94)
+    x = oracle.pivot_a_blocks(m, sizes, leaf_inverter=oracle.invertor_by_a)
+    assert x.tobytes() == GOLDEN["by_a_64"].tobytes()
+
+
+@pytest.mark.parametrize("sizes", [[8] * 8, [3, 9, 5, 11], [5, 7], [1], [256] * 16])
+def test_pivot_a_flops_are_2n3(sizes):
+    n = sum(sizes)
+    assert oracle.flops_pivot_a(sizes)["total"] == 2.0 * n**3
+
+
 def test_formulas_vs_golden():
     m = well_conditioned(60, 3)
     for nm, f in (("a", oracle.invert_via_a), ("d", oracle.invert_via_d), ("ad", oracle.invert_via_ad)):

@@ -8,6 +8,8 @@ residual ||A X - I||_F (K1 + K4).
   cfg5  n=65536, 256 x 256 blocks (--cfg5): run_inversion on ONE GPU
         (~138 GB of device state); input drawn on the device (torch
         Philox, seed 5) with the config's distribution, N(0,1)/256 + 4I
+  cfg4 and cfg5 also run the opt-in schedule="pivot_a" (2n^3 block-level
+  invertor_by_a recursion).
 """
 
 import argparse
@@ -94,23 +96,26 @@ def main():
 
     if "cfg4" not in skip:
         m, sizes = workloads.cfg4()
-        eng = bi.DeviceEngine(sizes, 1)
-        eng.load(m)
+        for sched in ("eq7", "pivot_a"):
+            eng = bi.DeviceEngine(sizes, 1, schedule=sched)
+            eng.load(m)
+            ms = time_engine(eng, 2)
+            fro, _ = _residual_device(eng.M, eng.Minv, batch=True)
+            c = eng.counters()
+            key = "cfg4" if sched == "eq7" else "cfg4_pivot_a"
+            out[key] = {"run_inversion_device_ms": ms, "tflops_nominal": 2 * 16384**3 / (ms * 1e-3) / 1e12,
+                        "tflops_algorithmic": (c["gemm_flops"] + c["leaf_flops"]) / (ms * 1e-3) / 1e12,
+                        "residual_fro": float(fro[0]), "schedule": sched}
+            print(key, out[key], flush=True)
+            del eng
+            torch.cuda.empty_cache()
         del m
-        ms = time_engine(eng, 2)
-        fro, _ = _residual_device(eng.M, eng.Minv, batch=True)
-        c = eng.counters()
-        out["cfg4"] = {"run_inversion_device_ms": ms, "tflops_nominal": 2 * 16384**3 / (ms * 1e-3) / 1e12,
-                       "tflops_algorithmic": (c["gemm_flops"] + c["leaf_flops"]) / (ms * 1e-3) / 1e12,
-                       "residual_fro": float(fro[0])}
-        print("cfg4", out["cfg4"], flush=True)
-        del eng
-        torch.cuda.empty_cache()
 
-    if args.cfg5:
+    for sched in (("eq7", "pivot_a") if args.cfg5 else ()):
         n = 65536
         sizes = [256] * 256
-        eng = bi.DeviceEngine(sizes, 1)
+        torch.cuda.reset_peak_memory_stats()
+        eng = bi.DeviceEngine(sizes, 1, schedule=sched)
         g = torch.Generator(device="cuda")
         g.manual_seed(5)
         for r0 in range(0, n, 4096):  # draw row chunks straight into M
@@ -123,11 +128,14 @@ def main():
         torch.cuda.synchronize()
         ms = time_engine(eng, 1)
         fro, mx = _residual_device(eng.M, eng.Minv, batch=True)
-        out["cfg5"] = {"run_inversion_device_s": ms / 1e3, "tflops_nominal": 2 * n**3 / (ms * 1e-3) / 1e12,
-                       "residual_fro": float(fro[0]), "residual_max": float(mx[0]),
-                       "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
-                       "input": "device-drawn N(0,1)/256 + 4I (torch Philox, seed 5)"}
-        print("cfg5", out["cfg5"], flush=True)
+        key = "cfg5" if sched == "eq7" else "cfg5_pivot_a"
+        out[key] = {"run_inversion_device_s": ms / 1e3, "tflops_nominal": 2 * n**3 / (ms * 1e-3) / 1e12,
+                    "residual_fro": float(fro[0]), "residual_max": float(mx[0]),
+                    "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9, "schedule": sched,
+                    "input": "device-drawn N(0,1)/256 + 4I (torch Philox, seed 5)"}
+        print(key, out[key], flush=True)
+        del eng
+        torch.cuda.empty_cache()
     print(json.dumps(out))
 
 
