@@ -133,6 +133,11 @@ int bi_engine_run_phase(bi_engine* e, int first_step, int last_step, int mask, v
  * GEMMs + leaf trailing updates), out[2] other K3 kernels. */
 int bi_engine_launches(const bi_engine* e, int first_step, int last_step, int64_t out[3]);
 int bi_engine_counters(const bi_engine* e, int first_step, int last_step, double out[6]);
+/* Profiling aid: with BI_ENGINE_TIMELINE=1 in the environment at bind time,
+ * every lane records a timing event after each step (graph runs included).
+ * After a run, out_ms[lane * (N_s + 1) + stepid] = ms from the run's start to
+ * the end of that step on that lane (-1 for steps outside the last run). */
+int bi_engine_timeline(bi_engine* e, float* out_ms);
 /* T-set access for step-state parity: pointer + ld of the level-`level`
  * provisional square of quad `quad` of matrix `matrix` (S_D at A's
  * position, R at B's, L at C's, S_A at D's; storage.py:166-262). */

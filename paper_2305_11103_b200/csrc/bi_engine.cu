@@ -180,6 +180,17 @@ struct bi_engine {
   int lane_priority[kMaxLanes] = {};
   int leaf_priority = 0;
   int gemm_cap = 0;  // engine GEMM grid cap (SMs left for the leaf chains)
+  int skew_mode = 1;  // lane start: 0 together, 1 after lane l-1's first step, 2 after lane 0's
+  struct Policy {
+    int lane_priority[kMaxLanes] = {};
+    int leaf_priority = 0;
+    int skew = 1;
+  } pol[2];  // [0] device-resident runs, [1] runs with host read-back
+  void set_policy(int i) {
+    for (int l = 0; l < kMaxLanes; ++l) lane_priority[l] = pol[i].lane_priority[l];
+    leaf_priority = pol[i].leaf_priority;
+    skew_mode = pol[i].skew;
+  }
   int zlo[kMaxLanes] = {}, zhi[kMaxLanes] = {};
   int* info = nullptr;
   GemmDesc* d_descs = nullptr;
@@ -195,7 +206,14 @@ struct bi_engine {
   cudaStream_t capture_stream = nullptr;
   cudaStream_t aux_stream[kMaxLanes] = {};  // lanes 1.. (lane 0 runs on the caller's stream)
   cudaEvent_t ev_fork = nullptr, ev_skew[kMaxLanes] = {}, ev_join[kMaxLanes] = {};
+  // BI_ENGINE_TIMELINE=1: timing events after every step of every lane
+  // (captured as external event-record nodes), read by bi_engine_timeline
+  bool timeline = false;
+  cudaEvent_t tl_start = nullptr;
+  std::vector<cudaEvent_t> tl_ev;  // [lane * (nsteps + 1) + stepid]
   cudaStream_t copy_stream = nullptr;       // host->device input copies
+  cudaStream_t d2h_stream[kMaxLanes] = {};  // per-lane read-back (page-locked output)
+  cudaEvent_t ev_d2h_a[kMaxLanes] = {}, ev_d2h_b[kMaxLanes] = {};
   std::vector<cudaEvent_t> ev_h2d;          // per (matrix, level): that level's input blocks copied
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int last_first = 1, last_last = 0;
@@ -212,7 +230,14 @@ struct bi_engine {
       if (ev_join[l]) cudaEventDestroy(ev_join[l]);
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (tl_start) cudaEventDestroy(tl_start);
+    for (cudaEvent_t ev : tl_ev) cudaEventDestroy(ev);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (int l = 0; l < kMaxLanes; ++l) {
+      if (d2h_stream[l]) cudaStreamDestroy(d2h_stream[l]);
+      if (ev_d2h_a[l]) cudaEventDestroy(ev_d2h_a[l]);
+      if (ev_d2h_b[l]) cudaEventDestroy(ev_d2h_b[l]);
+    }
     for (cudaEvent_t ev : ev_h2d) cudaEventDestroy(ev);
     if (meta_dev) cudaFree(meta_dev);
   }
@@ -608,13 +633,30 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   {
     // BI_PRIORITY_MODE: 0 none, 1 lane order (lane 0 highest), 2 leaf kernels
     // above GEMMs (default)
+    // Two scheduling policies (measured, profiles/r01_engine_policies.txt):
+    //  * device-resident runs: leaf kernels at the highest priority and lanes
+    //    chained one step apart (mode 2, skew 1) -- best step time;
+    //  * runs that read the inverses back to the host: lane 0 highest, lanes
+    //    start together (mode 1, skew 0) -- lanes finish staggered, so the
+    //    per-lane read-backs (PCIe-bound, ~2.3 ms each at cfg2) overlap compute.
+    // BI_PRIORITY_MODE / BI_ENGINE_SKEW override both.
     const char* pe = getenv("BI_PRIORITY_MODE");
-    const int mode = pe ? atoi(pe) : 2;
+    const char* sk = getenv("BI_ENGINE_SKEW");
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    for (int l = 0; l < e->nlanes; ++l)
-      e->lane_priority[l] = (mode == 1 && e->nlanes > 1) ? std::min(greatest + l, least) : 0;
-    e->leaf_priority = mode == 2 ? greatest : 0;
+    for (int pol = 0; pol < 2; ++pol) {
+      const int mode = pe ? atoi(pe) : (pol == 0 ? 2 : 1);
+      // mode 3: leaf kernels highest, then the GEMMs of later-starting lanes
+      for (int l = 0; l < e->nlanes; ++l) {
+        int pr = 0;
+        if (mode == 1 && e->nlanes > 1) pr = std::min(greatest + l, least);
+        if (mode == 3 && e->nlanes > 1) pr = std::min(greatest + 1 + (e->nlanes - 1 - l), least);
+        e->pol[pol].lane_priority[l] = pr;
+      }
+      e->pol[pol].leaf_priority = (mode == 2 || mode == 3) ? greatest : 0;
+      e->pol[pol].skew = sk ? atoi(sk) : (pol == 0 ? 1 : 0);
+    }
+    e->set_policy(0);
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -624,12 +666,29 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
     const int reserve = rs ? atoi(rs) : (e->nlanes > 1 ? 16 : 0);
     e->gemm_cap = (reserve > 0 && reserve < nsm) ? nsm - reserve : 0;
   }
+  if (!e->d2h_stream[0]) {
+    for (int l = 0; l < e->nlanes; ++l) {
+      BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->d2h_stream[l], cudaStreamNonBlocking));
+      BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_d2h_a[l], cudaEventDisableTiming));
+      BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_d2h_b[l], cudaEventDisableTiming));
+      if (!e->ev_join[l]) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_join[l], cudaEventDisableTiming));
+    }
+  }
   if (!e->copy_stream) {
     BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
     e->ev_h2d.assign((size_t)e->Z * (e->k + 1), nullptr);
     for (auto& ev : e->ev_h2d) BI_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   if (!e->ev_fork) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+  {
+    const char* tl = getenv("BI_ENGINE_TIMELINE");
+    e->timeline = tl && atoi(tl) != 0;
+    if (e->timeline && !e->tl_start) {
+      BI_CUDA_TRY(cudaEventCreate(&e->tl_start));
+      e->tl_ev.assign((size_t)e->nlanes * (e->nsteps + 1), nullptr);
+      for (auto& ev : e->tl_ev) BI_CUDA_TRY(cudaEventCreate(&ev));
+    }
+  }
   if (e->nlanes > 1 && !e->ev_skew[0]) {
     for (int l = 0; l < e->nlanes; ++l) {
       if (l > 0) BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->aux_stream[l], cudaStreamNonBlocking));
@@ -702,12 +761,17 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   return 0;
 }
 
+struct HostIO;
+static cudaError_t copy_top_quads(bi_engine* e, int lane, const HostIO* io, bool diag, cudaStream_t st);
+
 static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cudaStream_t s, int mask,
-                                cudaEvent_t after_first = nullptr, bool wait_input = false) {
+                                cudaEvent_t after_first = nullptr, bool wait_input = false,
+                                const HostIO* split_io = nullptr) {
   // Lane priority: lane 0 highest.  The leading lane then runs as if alone
   // and the others fill the SMs its latency-bound leaf phases leave idle.
   PriorityScope lane_prio(e->lane_priority[lane]);
   for (int stepid = first; stepid <= last; ++stepid) {
+    const auto& step_ops = e->lane_ops[lane][stepid];
     if (wait_input && (stepid & (stepid - 1)) == 0) {
       // Eq. 7: step 2^l is the first to read M at level l (diag blocks for
       // l = 0, the level-l quads' off-diagonal blocks for l >= 1).  pivot-A
@@ -721,9 +785,17 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
           if (err != cudaSuccess) return err;
         }
     }
-    for (const Op& op : e->lane_ops[lane][stepid]) {
+    for (const Op& op : step_ops) {
       if (!(mask & (op.kind == 0 ? 2 : 1))) continue;
       cudaError_t err;
+      if (split_io && stepid == e->nsteps && &op == &step_ops.back() && op.kind == 1) {
+        // last step, before its top-level up/down pass: the diagonal quads are
+        // final -- read them back while the pass runs
+        err = cudaEventRecord(e->ev_d2h_a[lane], s);
+        if (err == cudaSuccess) err = cudaStreamWaitEvent(e->d2h_stream[lane], e->ev_d2h_a[lane], 0);
+        if (err == cudaSuccess) err = copy_top_quads(e, lane, split_io, true, e->d2h_stream[lane]);
+        if (err != cudaSuccess) return err;
+      }
       if (op.kind == 2) {  // pivot-A: the lane's inputs into M_inv (inverted in place)
         err = cudaSuccess;
         for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z)
@@ -743,6 +815,11 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
       cudaError_t err = cudaEventRecord(after_first, s);
       if (err != cudaSuccess) return err;
     }
+    if (e->timeline) {
+      cudaError_t err = cudaEventRecordWithFlags(e->tl_ev[(size_t)lane * (e->nsteps + 1) + stepid], s,
+                                                 cudaEventRecordExternal);
+      if (err != cudaSuccess) return err;
+    }
   }
   return cudaSuccess;
 }
@@ -754,7 +831,30 @@ struct HostIO {
   int64_t ld_in, s_in;
   double* out;
   int64_t ld_out, s_out;
+  bool split_out = false;  // page-locked output of a full Eq. 7 run: read back in two halves
 };
+
+// Read-back of the quads of the top level: diag = the two diagonal quads (final
+// before the top-level up/down pass of the last step), else the two
+// off-diagonal quads (final after it).
+static cudaError_t copy_top_quads(bi_engine* e, int lane, const HostIO* io, bool diag, cudaStream_t st) {
+  cudaError_t err = cudaSuccess;
+  const int mid = e->nb / 2;
+  const int64_t h0 = e->off[mid], h1 = e->n - e->off[mid];
+  for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z) {
+    for (int part = 0; part < 2 && err == cudaSuccess; ++part) {
+      // diag: (0,0) [h0 x h0] and (h0,h0) [h1 x h1]; off: (0,h0) [h0 x h1] and (h0,0) [h1 x h0]
+      const int64_t r0 = part == 0 ? 0 : h0;
+      const int64_t c0 = diag ? r0 : (part == 0 ? h0 : 0);
+      const int64_t rows = part == 0 ? h0 : h1;
+      const int64_t cols = diag ? rows : (part == 0 ? h1 : h0);
+      err = cudaMemcpy2DAsync(io->out + (int64_t)z * io->s_out + r0 * io->ld_out + c0, io->ld_out * 8,
+                              e->Minv + (int64_t)z * e->si + r0 * e->ldi + c0, e->ldi * 8, cols * 8, rows,
+                              cudaMemcpyDeviceToHost, st);
+    }
+  }
+  return err;
+}
 
 static cudaError_t lane_io_pre(bi_engine* e, int lane, cudaStream_t ls, int first, const HostIO* io) {
   cudaError_t err = cudaSuccess;
@@ -768,6 +868,12 @@ static cudaError_t lane_io_pre(bi_engine* e, int lane, cudaStream_t ls, int firs
 static cudaError_t lane_io_post(bi_engine* e, int lane, cudaStream_t ls, const HostIO* io) {
   cudaError_t err = cudaSuccess;
   if (!io || !io->out) return err;
+  if (io->split_out) {  // the off-diagonal top quads, after the lane's last op
+    err = cudaEventRecord(e->ev_d2h_b[lane], ls);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(e->d2h_stream[lane], e->ev_d2h_b[lane], 0);
+    if (err == cudaSuccess) err = copy_top_quads(e, lane, io, false, e->d2h_stream[lane]);
+    return err;
+  }
   for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z)
     err = cudaMemcpy2DAsync(io->out + (int64_t)z * io->s_out, io->ld_out * 8, e->Minv + (int64_t)z * e->si,
                             e->ldi * 8, e->n * 8, e->n, cudaMemcpyDeviceToHost, ls);
@@ -777,8 +883,10 @@ static cudaError_t lane_io_post(bi_engine* e, int lane, cudaStream_t ls, const H
 static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s, int mask = 3,
                                  const HostIO* io = nullptr) {
   cudaError_t err = cudaSuccess;
+  e->set_policy(io && io->out ? 1 : 0);
   const bool fork = e->nlanes > 1 || (io && io->in);
-  if (fork) err = cudaEventRecord(e->ev_fork, s);
+  if (e->timeline) err = cudaEventRecordWithFlags(e->tl_start, s, cudaEventRecordExternal);
+  if (fork && err == cudaSuccess) err = cudaEventRecord(e->ev_fork, s);
   if (io && io->in && err == cudaSuccess) {
     // Input in level order across the batch: every matrix's diagonal blocks
     // (all step 1 reads), then level by level the quads' off-diagonal B and
@@ -827,19 +935,23 @@ static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t
     cudaStream_t ls = l == 0 ? s : e->aux_stream[l];
     if (l > 0) {
       err = cudaStreamWaitEvent(ls, e->ev_fork, 0);
-      if (err == cudaSuccess) err = cudaStreamWaitEvent(ls, e->ev_skew[l - 1], 0);
+      if (err == cudaSuccess && e->skew_mode == 1) err = cudaStreamWaitEvent(ls, e->ev_skew[l - 1], 0);
+      if (err == cudaSuccess && e->skew_mode == 2) err = cudaStreamWaitEvent(ls, e->ev_skew[0], 0);
     }
     if (err == cudaSuccess) err = lane_io_pre(e, l, ls, first, io);
     if (err == cudaSuccess)
-      err = enqueue_lane(e, l, first, last, ls, mask, e->nlanes > 1 ? e->ev_skew[l] : nullptr, io && io->in);
+      err = enqueue_lane(e, l, first, last, ls, mask, e->nlanes > 1 ? e->ev_skew[l] : nullptr, io && io->in,
+                         (io && io->split_out) ? io : nullptr);
   }
   // read-back after every lane is enqueued (a pageable D2H blocks the host)
+  const bool split = io && io->split_out;
   for (int l = 0; l < e->nlanes && err == cudaSuccess; ++l) {
     cudaStream_t ls = l == 0 ? s : e->aux_stream[l];
     err = lane_io_post(e, l, ls, io);
-    if (err == cudaSuccess && l > 0) err = cudaEventRecord(e->ev_join[l], ls);
+    if (err == cudaSuccess && (l > 0 || split)) err = cudaEventRecord(e->ev_join[l], split ? e->d2h_stream[l] : ls);
   }
-  for (int l = 1; l < e->nlanes && err == cudaSuccess; ++l) err = cudaStreamWaitEvent(s, e->ev_join[l], 0);
+  for (int l = split ? 0 : 1; l < e->nlanes && err == cudaSuccess; ++l)
+    err = cudaStreamWaitEvent(s, e->ev_join[l], 0);
   return err;
 }
 
@@ -858,6 +970,16 @@ static int run_impl(bi_engine* e, int first_step, int last_step, int use_graph, 
   e->last_first = first_step;
   e->last_last = last_step;
   if (io && !(is_pinned(io->in) && is_pinned(io->out))) use_graph = 0;  // pageable copies cannot be captured
+  HostIO io2;
+  if (io) {
+    io2 = *io;
+    // page-locked output of a full Eq. 7 run: the diagonal top quads are read
+    // back during the last step's top-level pass (a pageable D2H would block
+    // the host before the later lanes are enqueued)
+    io2.split_out = io->out && is_pinned(io->out) && io->out != nullptr && e->schedule == BI_SCHEDULE_EQ7 &&
+                    e->nb >= 2 && last_step == e->nsteps;
+    io = &io2;
+  }
   if (!use_graph) {
     BI_CUDA_TRY(enqueue_steps(e, first_step, last_step, s, 3, io));
     return 0;
@@ -918,6 +1040,23 @@ extern "C" int bi_engine_run_phase(bi_engine* e, int first_step, int last_step, 
   BI_REQUIRE(mask >= 1 && mask <= 3, "mask must be 1 (GEMM ops), 2 (leaf inversions) or 3");
   e->last_stream = static_cast<cudaStream_t>(stream);
   BI_CUDA_TRY(enqueue_steps(e, first_step, last_step, e->last_stream, mask));
+  return 0;
+}
+
+extern "C" int bi_engine_timeline(bi_engine* e, float* out_ms) {
+  BI_REQUIRE(e && e->bound && out_ms, "engine not bound");
+  BI_REQUIRE(e->timeline, "set BI_ENGINE_TIMELINE=1 before binding");
+  BI_CUDA_TRY(cudaStreamSynchronize(e->last_stream));
+  for (int l = 0; l < e->nlanes; ++l)
+    for (int st = 0; st <= e->nsteps; ++st) {
+      float v = -1.0f;
+      if (st >= e->last_first && st <= e->last_last &&
+          cudaEventElapsedTime(&v, e->tl_start, e->tl_ev[(size_t)l * (e->nsteps + 1) + st]) != cudaSuccess) {
+        cudaGetLastError();
+        v = -1.0f;
+      }
+      out_ms[(size_t)l * (e->nsteps + 1) + st] = v;
+    }
   return 0;
 }
 
