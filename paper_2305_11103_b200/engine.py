@@ -331,6 +331,63 @@ class DeviceEngine:
         return flat.as_strided((side.value, side.value), (ld.value, 1), off // 8)
 
 
+    # --- step-boundary state (checkpoint/resume) -------------------
+    def tset_levels_after(self, stepid: int) -> list[int]:
+        """Levels whose provisional entries exist after ``stepid`` (the
+        arrows step at level l stores every quad's L, R, S_D, S_A)."""
+        nb = len(self.sizes)
+        lv = set()
+        for st in range(1, stepid + 1):
+            a = decode_step(loopid_for_step(st, nb))
+            if a.sid is not None:
+                lv.add(a.sid)
+        return sorted(lv)
+
+    def _quad_spans(self, level: int, quad: int):
+        off = self.scheme.offsets
+        first = quad << level
+        mid = first + (1 << (level - 1))
+        last = (quad + 1) << level
+        return off[mid] - off[first], off[last] - off[mid]
+
+    def snapshot(self, stepid: int, matrix: int = 0):
+        """(M_inv dense, {level: {(kind, idx): array}}) of one matrix after
+        ``stepid`` -- the state the reference checkpoints (storage.py:292-328)."""
+        if self.schedule != "eq7":
+            raise ValueError("step-boundary state exists for the Eq. 7 schedule only")
+        minv = self.Minv[matrix, :, : self.n].cpu().numpy()
+        tsets = {}
+        for level in self.tset_levels_after(stepid):
+            entries = {}
+            for g in range(len(self.sizes) >> level):
+                ha, hd = self._quad_spans(level, g)
+                sq = self.tset_square(level, g, matrix).cpu().numpy()
+                entries[("L", g)] = np.ascontiguousarray(sq[ha:, :ha])
+                entries[("R", g)] = np.ascontiguousarray(sq[:ha, ha:])
+                entries[("S", 2 * g)] = np.ascontiguousarray(sq[:ha, :ha])
+                entries[("S", 2 * g + 1)] = np.ascontiguousarray(sq[ha:, ha:])
+            tsets[level] = entries
+        return minv, tsets
+
+    def restore(self, minv: np.ndarray, tsets: dict, matrix: int = 0) -> None:
+        """Upload a step-boundary state (inverse of ``snapshot``)."""
+        t = _lib.torch()
+        if self.schedule != "eq7":
+            raise ValueError("step-boundary state exists for the Eq. 7 schedule only")
+        self.Minv[matrix, :, : self.n].copy_(t.from_numpy(np.array(minv, dtype=np.float64)))
+        for level, entries in tsets.items():
+            for g in range(len(self.sizes) >> level):
+                ha, hd = self._quad_spans(level, g)
+                sq = self.tset_square(level, g, matrix)
+                for (kind, idx), rows, cols in ((("L", g), slice(ha, None), slice(0, ha)),
+                                                (("R", g), slice(0, ha), slice(ha, None)),
+                                                (("S", 2 * g), slice(0, ha), slice(0, ha)),
+                                                (("S", 2 * g + 1), slice(ha, None), slice(ha, None))):
+                    if (kind, idx) in entries:
+                        sq[rows, cols].copy_(t.from_numpy(np.array(entries[(kind, idx)], dtype=np.float64)))
+        t.cuda.synchronize()
+
+
 _ENGINES: "OrderedDict[tuple, DeviceEngine]" = OrderedDict()
 _CACHE_MAX = 2
 
@@ -383,16 +440,21 @@ def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backe
                   counters: OpCounters | None = None, *, schedule: str = "eq7") -> BlockMatrix:
     """Invert a partitioned matrix through the full step schedule on the B200
     (engine.py:482-542).  Same arguments and result type as the reference;
-    ``checkpoint_dir`` / ``file_backed`` (disk persistence, SURVEY 8f #3) are
-    not part of the device path and raise NotImplementedError.
+    ``checkpoint_dir`` / ``file_backed`` (step-boundary persistence) are
+    handled in the reference's on-disk format (checkpoint.py, SURVEY 8f #3).
     Extension: ``schedule="pivot_a"`` runs the same partition through the 2n^3
     block-level pivot-A recursion (invertor_by_a, recursive.py:83-123) instead
     of the Eq. 7 steps (SURVEY 8f #1); counters then follow invertor_by_a."""
     resolve_workers(workers)
     _check_schedule(schedule, stop_after_step)
-    if checkpoint_dir is not None or file_backed:
-        raise NotImplementedError("checkpoint/resume and file-backed stores are not on the B200 path")
+    if file_backed and checkpoint_dir is None:
+        raise ValueError("file-backed mode needs a checkpoint directory")  # storage.py:396-397
     scheme, dense = _scheme_and_dense(m, sizes)
+    if checkpoint_dir is not None:
+        if schedule != "eq7":
+            raise ValueError("checkpoints hold Eq. 7 step-boundary state; use schedule='eq7'")
+        return _run_checkpointed(scheme, np.ascontiguousarray(dense, dtype=np.float64), checkpoint_dir,
+                                 file_backed, stop_after_step, counters)
     eng = _engine_for(scheme.sizes, 1, schedule)
     last = _last_step(eng.n_steps, stop_after_step)
     dense = np.ascontiguousarray(dense, dtype=np.float64)
@@ -405,6 +467,45 @@ def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backe
         counters.inversions += c["inversions"]
         counters.reductions += c["reductions"]
     return BlockMatrix(scheme, MemoryBlockStore(scheme, out), role="inverse")
+
+
+def _run_checkpointed(scheme, dense, directory, file_backed, stop_after_step, counters) -> BlockMatrix:
+    """engine.py:515-542 with the device engine: resume a matching
+    checkpoint, then after every step snapshot M_inv and the stored
+    provisional entries into ``directory`` (reference format, checkpoint.py).
+    ``file_backed`` keeps the reference's directory semantics (stale block
+    files are dropped on a fresh start); the working state stays in HBM."""
+    from . import checkpoint as ckpt
+
+    sizes = list(scheme.sizes)
+    input_hash = ckpt.input_fingerprint(dense, sizes)
+    n_steps = total_steps(len(sizes))
+    eng = _engine_for(scheme.sizes, 1)
+    eng.load(dense)
+    start = 1
+    minv = None
+    if ckpt.has_checkpoint(directory):
+        meta = ckpt.checkpoint_load(directory)
+        ckpt.checkpoint_matches(meta, sizes, input_hash)
+        minv, tsets = ckpt.load_state(directory, sizes)
+        eng.restore(minv, tsets)
+        start = meta["stepid"] + 1
+    elif file_backed:
+        ckpt.clear_state(directory)
+    last = n_steps if stop_after_step is None else min(n_steps, max(start, int(stop_after_step)))
+    for stepid in range(start, last + 1):
+        eng.run(stepid, stepid, use_graph=False)
+        eng.check()
+        minv, tsets = eng.snapshot(stepid)
+        ckpt.checkpoint_save(directory, sizes, minv, tsets, stepid, input_hash)
+    if counters is not None and start <= last:
+        c = eng.counters(start, last)
+        counters.multiplies += c["multiplies"]
+        counters.inversions += c["inversions"]
+        counters.reductions += c["reductions"]
+    if minv is None:  # fresh start with nothing to run cannot happen (n_steps >= 1)
+        minv = eng.Minv[0, :, : eng.n].cpu().numpy()
+    return BlockMatrix(scheme, MemoryBlockStore(scheme, np.array(minv)), role="inverse")
 
 
 def run_inversion_batch(ms, sizes, out: np.ndarray | None = None,

@@ -93,6 +93,17 @@ def main():
                     for lv, t in ts.items():
                         for nm, arr in t.entries():
                             g[f"step8x8_tset_{lv}_{nm}"] = arr
+        # --- a checkpoint directory written by the reference (format parity,
+        #     SURVEY 8f #3): [8]*4, stopped after step 4 of 7; every file's bytes
+        for stop in (4,):
+            with tempfile.TemporaryDirectory() as d:
+                mc = well_conditioned(32, 61)
+                R.run_inversion(mc, sizes=[8] * 4, checkpoint_dir=d, stop_after_step=stop)
+                for path in sorted(Path(d).rglob("*")):
+                    if path.is_file():
+                        key = "ckpt4_file__" + str(path.relative_to(d)).replace("/", "__")
+                        g[key] = np.frombuffer(path.read_bytes(), dtype=np.uint8).copy()
+            g["ckpt4_final"] = R.run_inversion(mc, sizes=[8] * 4).to_dense()
         # --- recursive procedures and the GJ oracle
         for order in (8, 17, 64):
             m = well_conditioned(order, 30 + order)

@@ -181,8 +181,12 @@ def test_argument_errors_before_device(bi):
         bi.invert_small(np.eye(5), np.empty((5, 5)))
     with pytest.raises(bi.ScratchTooSmall):
         bi.invertor_inplace_by_a(np.eye(4), row_scratch=np.empty(2))
-    with pytest.raises(NotImplementedError):
-        bi.run_inversion(np.eye(4), checkpoint_dir="/tmp/x")
+    with pytest.raises(ValueError):  # storage.py:396-397
+        bi.run_inversion(np.eye(4), file_backed=True)
+    with pytest.raises(ValueError):
+        bi.run_inversion(np.eye(4), checkpoint_dir="/tmp/x", schedule="pivot_a")
+    with pytest.raises(bi.NativeUnavailable):  # checkpointed runs are device runs too: no CPU fallback
+        bi.run_inversion(np.eye(4), checkpoint_dir=str(ROOT / "gpurun_out" / "never_written"))
     with pytest.raises(ValueError):
         bi.run_inversion(np.eye(4), workers=0)
     with pytest.raises(bi.DimensionMismatch):

@@ -11,3 +11,12 @@ def cfg3_small(n=120, split=20, rank=10):
     m[:split, :split] = u @ v.T
     m[split:, split:] += float(n) * np.eye(n - split)
     return m
+
+
+def _load_golden():
+    from pathlib import Path
+
+    return np.load(Path(__file__).resolve().parent / "golden" / "golden.npz")
+
+
+GOLDEN = _load_golden()
