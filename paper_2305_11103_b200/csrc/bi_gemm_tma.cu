@@ -1,6 +1,17 @@
 // K1, TMA variant: D = [C] + sign * A * B with TMA-fed shared memory and an
 // mbarrier ring (no CTA-wide barrier in the main loop).
 //
+// Two ring managements (same tile, layout and summation order):
+//   gemm_tma_refill_kernel (default): the warp that releases a stage last
+//     refills it with the k-tile kStages ahead -- possibly the next tile's --
+//     so refills leave as early as possible and no warp waits for the
+//     slowest one;
+//   gemm_tma_kernel (BI_GEMM_REFILL=0): thread 0 produces kStages-1 ahead,
+//     waiting on per-stage "empty" barriers.
+// Measured on the same box (profiles/r01_k1_variants.txt): equal on plain
+// GEMMs, +0.9 % on accumulating ones, +0.5 % on the engine's K1 phase; a
+// deeper ring (6, 7 stages; BI_GEMM_STAGES) does not help.
+//
 // sm_100a has no tcgen05 FP64 kind; the FP64 tensor path is DMMA.8x8x4
 // (mma.sync.m8n8k4.f64).  This variant feeds it the Blackwell way: one thread
 // issues cp.async.bulk.tensor (TMA) loads of 128-byte-swizzled tiles into a
@@ -22,6 +33,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -30,13 +42,14 @@
 namespace bi {
 namespace {
 
-constexpr int kStages = 5;
+constexpr int kMaxStages = 7;  // 7 x 32 KB + slack fits the 227 KB of a CTA
 constexpr int kWarps = kK1Warps;
 constexpr int kThreads = kK1Threads;
 constexpr int kBoxBBytes = kK1BoxB;
 constexpr int kStageA = kK1StageA;
 constexpr int kStageBytes = kK1Stage;
-constexpr int kSmem = kStages * kStageBytes + 1024;  // + alignment slack
+template <int S>
+constexpr int smem_bytes() { return S * kStageBytes + 1024; }  // + alignment slack
 
 struct alignas(64) TmaLaunch {
   CUtensorMap ta[kGemmInline];
@@ -76,6 +89,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+template <int kStages>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_constant__ TmaLaunch L) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -138,6 +152,84 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_cons
   }
 }
 
+// Variant: no producer thread.  Each warp's lane 0 counts itself out of a
+// stage after consuming it; the warp that releases a stage last refills it
+// with the k-tile kStages ahead in the CTA's sequence (possibly the next
+// tile's).  Refills go out the moment a slot frees, nobody blocks on the
+// slowest warp, and the next tile's first loads overlap this tile's tail.
+template <int kStages>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tma_refill_kernel(const __grid_constant__ TmaLaunch L) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ unsigned released[kStages];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int fr = lane >> 2, fc = lane & 3;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  K1Frag f;
+  k1_frag_init(f, fr, fc);
+
+  // fill `stage` with the k-tile `ahead` positions past k-tile 0 of (tile, tc, KT)
+  auto fill = [&](int stage, int tile, K1Tile tc, int KT, int ahead) {
+    while (ahead >= KT) {
+      ahead -= KT;
+      tile += gridDim.x;
+      if (tile >= L.total_tiles) return;
+      tc = k1_locate(L.d, L.count, tile);
+      KT = (L.d[tc.desc].K + kBK - 1) / kBK;
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before async writes
+    uint8_t* sa = smem + stage * kStageBytes;
+    uint8_t* sb = sa + kStageA;
+    mbar_expect_tx(&full[stage], kStageBytes);
+    tma_load_3d(sa, &L.ta[tc.desc], &full[stage], ahead * kBK, tc.m0, tc.bz);
+#pragma unroll
+    for (int j = 0; j < kBN / 16; ++j)
+      tma_load_3d(sb + j * kBoxBBytes, &L.tb[tc.desc], &full[stage], tc.n0 + 16 * j, ahead * kBK, tc.bz);
+  };
+  if (tid == 0 && (int)blockIdx.x < L.total_tiles) {
+    const K1Tile t0 = k1_locate(L.d, L.count, blockIdx.x);
+    const int KT0 = (L.d[t0.desc].K + kBK - 1) / kBK;
+    for (int s = 0; s < kStages; ++s) fill(s, blockIdx.x, t0, KT0, s);
+  }
+
+  unsigned cons_it = 0;
+  for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
+    const K1Tile tc = k1_locate(L.d, L.count, tile);
+    const GemmDesc& d = L.d[tc.desc];
+    const int KT = (d.K + kBK - 1) / kBK;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+      const int stage = cons_it % kStages;
+      mbar_wait(&full[stage], (cons_it / kStages) & 1);
+      k1_compute(smem + stage * kStageBytes, f, wm, wn, fr, acc);
+      __syncwarp();
+      if (lane == 0 && atomicAdd(&released[stage], 1u) == kWarps - 1) {
+        released[stage] = 0;
+        fill(stage, tile, tc, KT, kt + kStages);
+      }
+      ++cons_it;
+    }
+
+    k1_epilogue(d, tc.bz, tc.m0, tc.n0, wm, wn, fr, fc, acc);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_tma_once;
 cudaError_t g_tma_err = cudaSuccess;
@@ -152,8 +244,20 @@ cudaError_t tma_init() {
       return;
     }
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel);
+    g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<5>());
+    if (g_tma_err == cudaSuccess)
+      g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<6>());
+    if (g_tma_err == cudaSuccess)
+      g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<7>());
+    if (g_tma_err == cudaSuccess)
+      g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_bytes<5>());
+    if (g_tma_err == cudaSuccess)
+      g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_bytes<6>());
+    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<5>);
+    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<6>);
+    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<7>);
   });
   return g_tma_err;
 }
@@ -196,7 +300,30 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
   L.total_tiles = total;
   if (total == 0) return true;
   const int grid = (grid_cap > 0 && grid_cap < total) ? grid_cap : total;
-  *err = launch_kernel(gemm_tma_kernel, dim3(grid), dim3(kThreads), (size_t)kSmem, stream, 1u, L);
+  static const int stages = [] {  // BI_GEMM_STAGES: TMA ring depth (5..7)
+    const char* e = getenv("BI_GEMM_STAGES");
+    const int v = e ? atoi(e) : 5;
+    return v < 5 ? 5 : (v > kMaxStages ? kMaxStages : v);
+  }();
+  static const int refill = [] {
+    const char* e = getenv("BI_GEMM_REFILL");
+    return e ? atoi(e) : 1;
+  }();
+  if (refill && stages <= 6) {
+    if (stages == 6)
+      *err = launch_kernel(gemm_tma_refill_kernel<6>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<6>(), stream,
+                           1u, L);
+    else
+      *err = launch_kernel(gemm_tma_refill_kernel<5>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<5>(), stream,
+                           1u, L);
+    return true;
+  }
+  if (stages == 7)
+    *err = launch_kernel(gemm_tma_kernel<7>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<7>(), stream, 1u, L);
+  else if (stages == 6)
+    *err = launch_kernel(gemm_tma_kernel<6>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<6>(), stream, 1u, L);
+  else
+    *err = launch_kernel(gemm_tma_kernel<5>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<5>(), stream, 1u, L);
   return true;
 }
 
