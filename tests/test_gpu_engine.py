@@ -325,3 +325,62 @@ def test_pivot_a_singular_leaf_and_arguments(bi):
     c = bi.OpCounters()
     bi.run_inversion(well_conditioned(16, 4), sizes=sizes, schedule="pivot_a", counters=c)
     assert (c.multiplies, c.inversions, c.reductions) == (18, 4, 6)
+
+
+# --- edge cases: late singular leaves, batches, NaN, one block, the largest leaf ---
+
+def test_singular_schur_complement_reported_at_its_step(bi):
+    """S_D = A - B D^-1 C = 0 in quad 0 of level 1: the leaf inverted at step 3
+    (diag from T1) is singular; the device reports the oracle's (step, quad)."""
+    m = np.eye(16)
+    m[0:4, 4:8] = np.eye(4)
+    m[4:8, 0:4] = np.eye(4)
+    with pytest.raises(oracle.OracleSingular) as ref:
+        oracle.run_inversion(m, sizes=[4] * 4, leaf_inverter=oracle.gauss_jordan)
+    with pytest.raises(bi.SingularBlock) as got:
+        bi.run_inversion(m, sizes=[4] * 4)
+    assert (got.value.step, got.value.quad) == (ref.value.step, ref.value.quad) == (3, 0)
+
+
+def test_batch_reports_the_singular_matrix(bi):
+    ms = np.stack([well_conditioned(64, 70 + i) for i in range(3)])
+    ms[1, :8, :8] = 1.0  # rank-1 first leaf of matrix 1
+    with pytest.raises(bi.SingularBlock) as got:
+        bi.run_inversion_batch(ms, [8] * 8)
+    assert got.value.step == 1 and got.value.quad == 0 and got.value.matrix == 1
+
+
+def test_nan_input_propagates_like_the_reference(bi):
+    """NaN ranks as the pivot (numpy.argmax) and never trips the singular
+    test (NaN <= tol is false): the result is NaN, no exception, no hang."""
+    m = well_conditioned(32, 71)
+    m[3, 5] = np.nan
+    ref = oracle.run_inversion(m, sizes=[8] * 4, leaf_inverter=oracle.gauss_jordan)
+    got = bi.run_inversion(m, sizes=[8] * 4).to_dense()
+    assert np.isnan(ref).any() and np.isnan(got).any()
+
+
+def test_single_block_partition(bi):
+    m = well_conditioned(100, 72)
+    got = bi.run_inversion(m, sizes=[100]).to_dense()
+    _assert_ref_criteria(m, got, oracle.gauss_jordan(m))
+
+
+def test_largest_leaf_order_8192(bi):
+    """K3 at its limit (n = 8192: a 16-CTA cluster per block), checked by the
+    device residual (K1 + K4, itself checked against NumPy in test_gpu_kernels)."""
+    import torch
+
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.core import _residual_device, device_inverse
+
+    n = 8192
+    g = torch.Generator(device="cuda")
+    g.manual_seed(8192)
+    a = torch.randn((1, n, n), generator=g, dtype=torch.float64, device="cuda") / np.sqrt(n)
+    a[0].diagonal().add_(2.0)
+    x = _lib.empty_matrix(n, n, batch=1)
+    info = device_inverse(a, x)
+    assert (info == 0).all()
+    fro, mx = _residual_device(a, x, batch=True)
+    assert fro[0] <= 1e-9 * n and mx[0] <= 1e-10
