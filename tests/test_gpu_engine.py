@@ -384,3 +384,23 @@ def test_largest_leaf_order_8192(bi):
     assert (info == 0).all()
     fro, mx = _residual_device(a, x, batch=True)
     assert fro[0] <= 1e-9 * n and mx[0] <= 1e-10
+
+
+def test_batch_wider_than_the_lanes(bi):
+    """Batch 10 on 8 lanes (two lanes carry two matrices): device-resident and
+    page-locked host paths equal the single-matrix runs bitwise."""
+    import torch
+
+    sizes = [16] * 8
+    ms = np.stack([well_conditioned(128, 80 + i) for i in range(10)])
+    single = np.stack([bi.run_inversion(ms[i], sizes=sizes).to_dense() for i in range(10)])
+    assert np.array_equal(bi.run_inversion_batch(ms, sizes), single)
+    pin_in = torch.from_numpy(ms).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+    bi.run_inversion_batch(pin_in.numpy(), sizes, out=pin_out.numpy())
+    assert np.array_equal(pin_out.numpy(), single)
+    eng = bi.DeviceEngine(sizes, batch=10)
+    eng.load(ms)
+    eng.run()
+    eng.check()
+    assert np.array_equal(eng.Minv[:, :, :128].cpu().numpy(), single)
