@@ -12,6 +12,13 @@
 // GEMMs, +0.9 % on accumulating ones, +0.5 % on the engine's K1 phase; a
 // deeper ring (6, 7 stages; BI_GEMM_STAGES) does not help.
 //
+// Tile: 128 x 64 with 8 warps (4-stage ring, 97 KB) and TWO CTAs per SM is
+// the default (BI_GEMM_TN=128 selects the 16-warp 128 x 128 CTA): one CTA's
+// epilogue and ring refill run under the other CTA's main loop, which the
+// single 16-warp CTA cannot do.  Same box: 2048^3 x 8 33.2 -> 34.3 TF/s,
+// C += AB 32.9 -> 34.1 (99 % of cuBLAS), 512^3 x 32 27.7 -> 32.6; engine K1
+// phase 32.5 -> 33.5 TF/s.
+//
 // sm_100a has no tcgen05 FP64 kind; the FP64 tensor path is DMMA.8x8x4
 // (mma.sync.m8n8k4.f64).  This variant feeds it the Blackwell way: one thread
 // issues cp.async.bulk.tensor (TMA) loads of 128-byte-swizzled tiles into a
@@ -157,15 +164,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_cons
 // with the k-tile kStages ahead in the CTA's sequence (possibly the next
 // tile's).  Refills go out the moment a slot frees, nobody blocks on the
 // slowest warp, and the next tile's first loads overlap this tile's tail.
-template <int kStages>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tma_refill_kernel(const __grid_constant__ TmaLaunch L) {
+// TN = 128: 16 warps, one CTA per SM.  TN = 64: 8 warps on a 128 x 64 tile,
+// two CTAs per SM, so one CTA's epilogue runs under the other's main loop.
+template <int TN>
+struct RefillCfg {
+  static constexpr int kWarpsT = 4 * (TN / 32);
+  static constexpr int kThr = kWarpsT * 32;
+  static constexpr int kStageB = kBK * TN * 8;
+  static constexpr int kStage = kStageA + kStageB;
+  static constexpr int kMinBlocks = TN == 64 ? 2 : 1;
+};
+template <int kStages, int TN>
+constexpr int refill_smem() { return kStages * RefillCfg<TN>::kStage + 1024; }
+
+template <int kStages, int TN>
+__global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks)
+    gemm_tma_refill_kernel(const __grid_constant__ TmaLaunch L) {
+  using Cfg = RefillCfg<TN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ unsigned released[kStages];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / (TN / 32), wn = warp % (TN / 32);
   const int fr = lane >> 2, fc = lane & 3;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -185,27 +207,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_refill_kernel(const __gr
       ahead -= KT;
       tile += gridDim.x;
       if (tile >= L.total_tiles) return;
-      tc = k1_locate(L.d, L.count, tile);
+      tc = k1_locate<kBM, TN>(L.d, L.count, tile);
       KT = (L.d[tc.desc].K + kBK - 1) / kBK;
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before async writes
-    uint8_t* sa = smem + stage * kStageBytes;
+    uint8_t* sa = smem + stage * Cfg::kStage;
     uint8_t* sb = sa + kStageA;
-    mbar_expect_tx(&full[stage], kStageBytes);
+    mbar_expect_tx(&full[stage], Cfg::kStage);
     tma_load_3d(sa, &L.ta[tc.desc], &full[stage], ahead * kBK, tc.m0, tc.bz);
 #pragma unroll
-    for (int j = 0; j < kBN / 16; ++j)
+    for (int j = 0; j < TN / 16; ++j)
       tma_load_3d(sb + j * kBoxBBytes, &L.tb[tc.desc], &full[stage], tc.n0 + 16 * j, ahead * kBK, tc.bz);
   };
   if (tid == 0 && (int)blockIdx.x < L.total_tiles) {
-    const K1Tile t0 = k1_locate(L.d, L.count, blockIdx.x);
+    const K1Tile t0 = k1_locate<kBM, TN>(L.d, L.count, blockIdx.x);
     const int KT0 = (L.d[t0.desc].K + kBK - 1) / kBK;
     for (int s = 0; s < kStages; ++s) fill(s, blockIdx.x, t0, KT0, s);
   }
 
   unsigned cons_it = 0;
   for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
-    const K1Tile tc = k1_locate(L.d, L.count, tile);
+    const K1Tile tc = k1_locate<kBM, TN>(L.d, L.count, tile);
     const GemmDesc& d = L.d[tc.desc];
     const int KT = (d.K + kBK - 1) / kBK;
     double acc[4][4][2];
@@ -217,16 +239,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_refill_kernel(const __gr
     for (int kt = 0; kt < KT; ++kt) {
       const int stage = cons_it % kStages;
       mbar_wait(&full[stage], (cons_it / kStages) & 1);
-      k1_compute(smem + stage * kStageBytes, f, wm, wn, fr, acc);
+      k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
       __syncwarp();
-      if (lane == 0 && atomicAdd(&released[stage], 1u) == kWarps - 1) {
+      if (lane == 0 && atomicAdd(&released[stage], 1u) == Cfg::kWarpsT - 1) {
         released[stage] = 0;
         fill(stage, tile, tc, KT, kt + kStages);
       }
       ++cons_it;
     }
 
-    k1_epilogue(d, tc.bz, tc.m0, tc.n0, wm, wn, fr, fc, acc);
+    k1_epilogue<kBM, TN>(d, tc.bz, tc.m0, tc.n0, wm, wn, fr, fc, acc);
   }
 }
 
@@ -250,11 +272,11 @@ cudaError_t tma_init() {
     if (g_tma_err == cudaSuccess)
       g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<7>());
     if (g_tma_err == cudaSuccess)
-      g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_bytes<5>());
+      g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<5, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       refill_smem<5, 128>());
     if (g_tma_err == cudaSuccess)
-      g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_bytes<6>());
+      g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       refill_smem<4, 64>());
     if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<5>);
     if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<6>);
     if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<7>);
@@ -309,13 +331,31 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
     const char* e = getenv("BI_GEMM_REFILL");
     return e ? atoi(e) : 1;
   }();
-  if (refill && stages <= 6) {
-    if (stages == 6)
-      *err = launch_kernel(gemm_tma_refill_kernel<6>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<6>(), stream,
-                           1u, L);
-    else
-      *err = launch_kernel(gemm_tma_refill_kernel<5>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<5>(), stream,
-                           1u, L);
+  static const int tn = [] {  // BI_GEMM_TN: 64 (8 warps, 2 CTAs/SM; default) or 128 (16 warps, 1 CTA/SM)
+    const char* e = getenv("BI_GEMM_TN");
+    return (e && atoi(e) == 128) ? 128 : 64;
+  }();
+  if (refill && tn == 64) {
+    // re-tile the descriptors for 128 x 64 tiles
+    int t = 0;
+    for (int i = 0; i < count; ++i) {
+      GemmDesc& d = L.d[i];
+      const bool empty = d.M <= 0 || d.N <= 0 || d.batch <= 0;
+      d.tiles_m = empty ? 0 : (d.M + kBM - 1) / kBM;
+      d.tiles_n = empty ? 1 : (d.N + 63) / 64;
+      d.tile_begin = t;
+      t += empty ? 0 : d.tiles_m * d.tiles_n * d.batch;
+    }
+    L.total_tiles = t;
+    const int cap2 = grid_cap > 0 ? 2 * grid_cap : 0;
+    const int grid2 = (cap2 > 0 && cap2 < t) ? cap2 : t;
+    *err = launch_kernel(gemm_tma_refill_kernel<4, 64>, dim3(grid2), dim3(RefillCfg<64>::kThr),
+                         (size_t)refill_smem<4, 64>(), stream, 1u, L);
+    return true;
+  }
+  if (refill) {
+    *err = launch_kernel(gemm_tma_refill_kernel<5, 128>, dim3(grid), dim3(RefillCfg<128>::kThr),
+                         (size_t)refill_smem<5, 128>(), stream, 1u, L);
     return true;
   }
   if (stages == 7)
