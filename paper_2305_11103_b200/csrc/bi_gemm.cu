@@ -207,13 +207,14 @@ __global__ void __launch_bounds__(K1Cfg<TM, TN>::kThreads) gemm_dmma_kernel(cons
 std::once_flag g_attr_once;
 cudaError_t g_attr_err = cudaSuccess;
 
-int small_tile_threshold() {  // BI_GEMM_SMALL_TILES: 128-tile count below which 64 x 64 tiles are used
+// BI_GEMM_SMALL_TILES: 128-tile count below which a launch runs on the 64 x 64
+// cp.async latency tiles.  Default 0 (off): since the TMA kernel runs 128 x 64
+// tiles two CTAs per SM, it is as good on small launches and better in the
+// engine (bench 29.1 -> 28.0 ms; profiles/r01_k1_variants.txt).
+int small_tile_threshold() {
   static const int v = [] {
     const char* e = getenv("BI_GEMM_SMALL_TILES");
-    if (e) return atoi(e);
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms;
+    return e ? atoi(e) : 0;
   }();
   return v;
 }
@@ -263,8 +264,7 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
   const int total =
       last.tile_begin + ((last.M <= 0 || last.N <= 0 || last.batch <= 0) ? 0 : last.tiles_m * last.tiles_n * last.batch);
   if (total == 0) return cudaSuccess;
-  // Launches whose 128-tile grid cannot fill the GPU are latency-bound (one
-  // FP64 SM needs ~4 us per 128 x 128 x 16 k-tile): 64 x 64 tiles, 4x the CTAs.
+  // Optional latency tiles for launches whose 128-tile grid cannot fill the GPU.
   if (count <= kGemmInline && total < small_tile_threshold()) return launch_gemm_small_n(h_descs, count, stream);
   if (use_tma()) {
     cudaError_t te = cudaSuccess;
