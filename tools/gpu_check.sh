@@ -1,1 +1,7 @@
-for th in 148 0 74 148 0; do echo "small-threshold $th"; for c in 8 32; do BI_GEMM_SMALL_TILES=$th python tools/profile_inv.py --count $c; done 2>&1 | tail -2; BI_GEMM_SMALL_TILES=$th python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b39.json 2> gpurun_out/b39.err; python -c "import json; d=json.load(open('gpurun_out/b39.json')); print('  bench value', round(d['value'],2), 'ms', round(d['ms_per_step'],2), 'e2e_ms', round(d['e2e']['ms_per_step'],2), 'k1', round(d['roofline']['achieved'],2))"; done
+python tools/gemm_sweep.py --profile 2 > /dev/null 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:gemm_tma -c 1 -o gpurun_out/r01_k1_tma_n64 python tools/gemm_sweep.py --profile 2 > gpurun_out/p_ncu2.log 2>&1
+python tools/k1_traffic.py run > gpurun_out/t_plain.log 2>&1 && \
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    --nvtx --nvtx-include k1_phase/ --csv --log-file gpurun_out/k1_traffic.csv \
+    python tools/k1_traffic.py run > gpurun_out/t_ncu.log 2>&1
+tail -n 1 gpurun_out/p_ncu2.log gpurun_out/t_ncu.log
