@@ -634,8 +634,9 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
     // BI_PRIORITY_MODE: 0 none, 1 lane order (lane 0 highest), 2 leaf kernels
     // above GEMMs (default)
     // Two scheduling policies (measured, profiles/r01_engine_policies.txt):
-    //  * device-resident runs: leaf kernels at the highest priority and lanes
-    //    chained one step apart (mode 2, skew 1) -- best step time;
+    //  * device-resident runs: leaf kernels at the highest priority, then the
+    //    GEMMs in lane order; lanes start together (mode 4, skew 0) -- best
+    //    step time with the two-CTA K1 (mode 2 / skew 1 before it);
     //  * runs that read the inverses back to the host: lane 0 highest, lanes
     //    start together (mode 1, skew 0) -- lanes finish staggered, so the
     //    per-lane read-backs (PCIe-bound, ~2.3 ms each at cfg2) overlap compute.
@@ -645,7 +646,7 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
     for (int pol = 0; pol < 2; ++pol) {
-      const int mode = pe ? atoi(pe) : (pol == 0 ? 2 : 1);
+      const int mode = pe ? atoi(pe) : (pol == 0 ? 4 : 1);
       // mode 3: leaf kernels highest, then the GEMMs of later-starting lanes
       for (int l = 0; l < e->nlanes; ++l) {
         int pr = 0;
@@ -654,7 +655,7 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
         e->pol[pol].lane_priority[l] = pr;
       }
       e->pol[pol].leaf_priority = (mode == 2 || mode == 3) ? greatest : 0;
-      e->pol[pol].skew = sk ? atoi(sk) : (pol == 0 ? 1 : 0);
+      e->pol[pol].skew = sk ? atoi(sk) : 0;
     }
     e->set_policy(0);
     int dev = 0, nsm = 0;
