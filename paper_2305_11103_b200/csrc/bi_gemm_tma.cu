@@ -10,7 +10,7 @@
 //     waiting on per-stage "empty" barriers.
 // Measured on the same box (profiles/r01_k1_variants.txt): equal on plain
 // GEMMs, +0.9 % on accumulating ones, +0.5 % on the engine's K1 phase; a
-// deeper ring (6, 7 stages; BI_GEMM_STAGES) does not help.
+// deeper ring (6, 7 stages) did not help.
 //
 // Tile: 128 x 64 with 8 warps (4-stage ring, 97 KB) and TWO CTAs per SM is
 // the default (BI_GEMM_TN=128 selects the 16-warp 128 x 128 CTA): one CTA's
@@ -49,7 +49,6 @@
 namespace bi {
 namespace {
 
-constexpr int kMaxStages = 7;  // 7 x 32 KB + slack fits the 227 KB of a CTA
 constexpr int kWarps = kK1Warps;
 constexpr int kThreads = kK1Threads;
 constexpr int kBoxBBytes = kK1BoxB;
@@ -268,18 +267,14 @@ cudaError_t tma_init() {
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<5>());
     if (g_tma_err == cudaSuccess)
-      g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<6>());
-    if (g_tma_err == cudaSuccess)
-      g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<7>());
-    if (g_tma_err == cudaSuccess)
       g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<5, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        refill_smem<5, 128>());
     if (g_tma_err == cudaSuccess)
       g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        refill_smem<4, 64>());
     if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<5>);
-    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<6>);
-    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<7>);
+    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_refill_kernel<5, 128>);
+    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_refill_kernel<4, 64>);
   });
   return g_tma_err;
 }
@@ -322,11 +317,6 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
   L.total_tiles = total;
   if (total == 0) return true;
   const int grid = (grid_cap > 0 && grid_cap < total) ? grid_cap : total;
-  static const int stages = [] {  // BI_GEMM_STAGES: TMA ring depth (5..7)
-    const char* e = getenv("BI_GEMM_STAGES");
-    const int v = e ? atoi(e) : 5;
-    return v < 5 ? 5 : (v > kMaxStages ? kMaxStages : v);
-  }();
   static const int refill = [] {
     const char* e = getenv("BI_GEMM_REFILL");
     return e ? atoi(e) : 1;
@@ -358,12 +348,7 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
                          (size_t)refill_smem<5, 128>(), stream, 1u, L);
     return true;
   }
-  if (stages == 7)
-    *err = launch_kernel(gemm_tma_kernel<7>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<7>(), stream, 1u, L);
-  else if (stages == 6)
-    *err = launch_kernel(gemm_tma_kernel<6>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<6>(), stream, 1u, L);
-  else
-    *err = launch_kernel(gemm_tma_kernel<5>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<5>(), stream, 1u, L);
+  *err = launch_kernel(gemm_tma_kernel<5>, dim3(grid), dim3(kThreads), (size_t)smem_bytes<5>(), stream, 1u, L);
   return true;
 }
 
