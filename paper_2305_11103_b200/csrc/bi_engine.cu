@@ -803,6 +803,11 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
           err = cudaMemcpy2DAsync(e->Minv + (int64_t)z * e->si, e->ldi * 8, e->M + (int64_t)z * e->sm, e->ldm * 8,
                                   e->n * 8, e->n, cudaMemcpyDeviceToDevice, s);
       } else if (op.kind == 0) {
+        static const bool skip_leaves = [] {  // timing experiments only: results are wrong
+          const char* v = getenv("BI_DEBUG_SKIP_LEAVES");
+          return v && atoi(v) != 0;
+        }();
+        if (skip_leaves) continue;
         PriorityScope leaf_prio(e->leaf_priority ? e->leaf_priority : g_launch_priority);
         err = launch_inv_group(e->invs[op.index].g, s);
       } else {
