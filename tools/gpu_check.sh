@@ -1,7 +1,4 @@
-python tools/gemm_sweep.py --profile 2 > /dev/null 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:gemm_tma -c 1 -o gpurun_out/r01_k1_tma_n64 python tools/gemm_sweep.py --profile 2 > gpurun_out/p_ncu2.log 2>&1
-python tools/k1_traffic.py run > gpurun_out/t_plain.log 2>&1 && \
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    --nvtx --nvtx-include k1_phase/ --csv --log-file gpurun_out/k1_traffic.csv \
-    python tools/k1_traffic.py run > gpurun_out/t_ncu.log 2>&1
-tail -n 1 gpurun_out/p_ncu2.log gpurun_out/t_ncu.log
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -m gpu -q -x 2>&1 | tail -1
+for c in 8 32; do python tools/profile_inv_graph.py --count $c; done; python tools/profile_inv_graph.py --count 64 --n 256
+python tools/profile_inv.py --count 1 --n 5000 2>&1 | tail -1
+for i in 1 2; do python bench.py --steps 8 --warmup 3 --no-cpu-baseline > gpurun_out/b41.json 2> gpurun_out/b41.err; python -c "import json; d=json.load(open('gpurun_out/b41.json')); print('value', round(d['value'],2), 'ms', round(d['ms_per_step'],2), 'e2e_ms', round(d['e2e']['ms_per_step'],2))"; done
