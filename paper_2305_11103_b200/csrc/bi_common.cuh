@@ -1,6 +1,9 @@
 // Shared definitions for the B200 blockwise-inversion library (sm_100a only).
 #pragma once
 
+#include <mutex>
+#include <vector>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -78,6 +81,24 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
                         cudaStream_t stream);
 // One descriptor on 64 x 64 tiles (latency path; same summation order).
 cudaError_t launch_gemm_small(const GemmDesc& h, cudaStream_t stream);
+
+// Run `fn` once per CUDA device and cache its status: kernel attributes
+// (dynamic shared memory limits, carveouts, cluster permissions) are per
+// device, so a process driving several GPUs must set them on each.
+struct PerDeviceOnce {
+  std::mutex mu;
+  std::vector<int> status;  // -1 unset, else the cudaError_t of the first run
+  template <typename F>
+  cudaError_t run(F fn) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)status.size() <= dev) status.resize(dev + 1, -1);
+    if (status[dev] < 0) status[dev] = (int)fn();
+    return (cudaError_t)status[dev];
+  }
+};
 
 // Preferred L1/shared carveout (percent) applied to every kernel of the
 // library, from BI_CARVEOUT (default -1 = driver default).

@@ -204,8 +204,6 @@ __global__ void __launch_bounds__(K1Cfg<TM, TN>::kThreads) gemm_dmma_kernel(cons
   }
 }
 
-std::once_flag g_attr_once;
-cudaError_t g_attr_err = cudaSuccess;
 
 // BI_GEMM_SMALL_TILES: 128-tile count below which a launch runs on the 64 x 64
 // cp.async latency tiles.  Default 0 (off): since the TMA kernel runs 128 x 64
@@ -242,16 +240,17 @@ int finalize_descs(GemmDesc* d, int count) {
 }
 
 cudaError_t gemm_init_attributes() {
-  std::call_once(g_attr_once, [] {
-    g_attr_err = cudaFuncSetAttribute(gemm_dmma_kernel<kBM, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      K1Cfg<kBM, kBN>::kSmem);
-    if (g_attr_err == cudaSuccess)
-      g_attr_err = cudaFuncSetAttribute(gemm_dmma_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        K1Cfg<64, 64>::kSmem);
-    if (g_attr_err == cudaSuccess) g_attr_err = set_carveout(gemm_dmma_kernel<kBM, kBN>);
-    if (g_attr_err == cudaSuccess) g_attr_err = set_carveout(gemm_dmma_kernel<64, 64>);
+  static PerDeviceOnce once;
+  return once.run([] {
+    cudaError_t e = cudaFuncSetAttribute(gemm_dmma_kernel<kBM, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         K1Cfg<kBM, kBN>::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_dmma_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               K1Cfg<64, 64>::kSmem);
+    if (e == cudaSuccess) e = set_carveout(gemm_dmma_kernel<kBM, kBN>);
+    if (e == cudaSuccess) e = set_carveout(gemm_dmma_kernel<64, 64>);
+    return e;
   });
-  return g_attr_err;
 }
 
 cudaError_t launch_gemm_small_n(const GemmDesc* h, int count, cudaStream_t stream);

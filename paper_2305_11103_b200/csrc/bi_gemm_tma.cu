@@ -256,7 +256,7 @@ std::once_flag g_tma_once;
 cudaError_t g_tma_err = cudaSuccess;
 
 cudaError_t tma_init() {
-  std::call_once(g_tma_once, [] {
+  std::call_once(g_tma_once, [] {  // the driver entry point: once per process
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
     cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
@@ -265,18 +265,23 @@ cudaError_t tma_init() {
       return;
     }
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    g_tma_err = cudaFuncSetAttribute(gemm_tma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<5>());
-    if (g_tma_err == cudaSuccess)
-      g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<5, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       refill_smem<5, 128>());
-    if (g_tma_err == cudaSuccess)
-      g_tma_err = cudaFuncSetAttribute(gemm_tma_refill_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       refill_smem<4, 64>());
-    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_kernel<5>);
-    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_refill_kernel<5, 128>);
-    if (g_tma_err == cudaSuccess) g_tma_err = set_carveout(gemm_tma_refill_kernel<4, 64>);
   });
-  return g_tma_err;
+  if (g_tma_err != cudaSuccess) return g_tma_err;
+  static PerDeviceOnce attrs;  // kernel attributes: once per device
+  return attrs.run([] {
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_tma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<5>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_tma_refill_kernel<5, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               refill_smem<5, 128>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_tma_refill_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               refill_smem<4, 64>());
+    if (e == cudaSuccess) e = set_carveout(gemm_tma_kernel<5>);
+    if (e == cudaSuccess) e = set_carveout(gemm_tma_refill_kernel<5, 128>);
+    if (e == cudaSuccess) e = set_carveout(gemm_tma_refill_kernel<4, 64>);
+    return e;
+  });
 }
 
 bool encode_3d(CUtensorMap* map, const double* base, uint64_t inner, uint64_t outer, uint64_t batch, int64_t ld,

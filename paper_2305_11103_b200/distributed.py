@@ -69,8 +69,9 @@ def _group_ranks(rank: int, group_size: int) -> list[int]:
 class ShardedEngine:
     """One rank's share of the step engine for ``sizes`` over a process group."""
 
-    def __init__(self, sizes, group=None, backend=None):
-        import torch.distributed as dist
+    def __init__(self, sizes, group=None, backend=None, dist=None):
+        if dist is None:  # a LocalDist facade (local_group.py) drives P GPUs from one process
+            import torch.distributed as dist
 
         self.dist = dist
         self.group = group if group is not None else dist.group.WORLD
@@ -182,7 +183,7 @@ class ShardedEngine:
         import torch
 
         send = send.contiguous()
-        if self.dist.get_backend(pg) == "nccl":
+        if self.dist.get_backend(pg) in ("nccl", "local"):
             recv = torch.empty((size,) + tuple(send.shape), dtype=send.dtype, device=send.device)
             self.dist.all_gather_into_tensor(recv, send, group=pg)
             return recv
@@ -345,13 +346,30 @@ class ShardedEngine:
         return torch.cat([recv[r][:, :self._width(r)] for r in range(self.P)], dim=1).cpu().numpy()
 
 
-def run_inversion_sharded(m, sizes, group=None, backend=None, stop_after_step=None) -> np.ndarray:
+def run_inversion_sharded(m, sizes, group=None, backend=None, stop_after_step=None, dist=None) -> np.ndarray:
     """run_inversion (engine.py:482-542) with the matrix column-sharded over the
-    ranks of ``group`` (one process per GPU).  Every rank passes the same
-    ``m``; every rank receives the full inverse.  Raises SingularBlock like the
+    ranks of ``group`` (one process per GPU, or one thread per GPU with a
+    local_group facade as ``dist``).  Every rank passes the same ``m``; every
+    rank receives the full inverse.  Raises SingularBlock like the
     single-device engine."""
-    eng = ShardedEngine(sizes, group=group, backend=backend)
+    eng = ShardedEngine(sizes, group=group, backend=backend, dist=dist)
     eng.load(np.asarray(m, dtype=np.float64))
     eng.run(1, stop_after_step)
     eng.check()
     return eng.gather()
+
+
+def run_inversion_local(m, sizes, gpus: int, stop_after_step=None, devices=None, backend_factory=None) -> np.ndarray:
+    """The sharded schedule on ``gpus`` GPUs of THIS process (one thread per
+    GPU, slabs exchanged by peer copies; local_group.py).  ``devices``
+    overrides the thread -> device map (tests run several "GPUs" on one);
+    ``backend_factory`` replaces the device backend (CPU tests)."""
+    from .local_group import run_threads
+
+    m = np.asarray(m, dtype=np.float64)
+
+    def target(dist, rank):
+        be = backend_factory() if backend_factory is not None else None
+        return run_inversion_sharded(m, sizes, backend=be, stop_after_step=stop_after_step, dist=dist)
+
+    return run_threads(gpus, target, devices=devices)[0]

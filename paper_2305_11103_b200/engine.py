@@ -40,8 +40,9 @@ SCHUR_DIAG_AND_ASSEMBLE = "schur_diag_and_assemble"
 
 def resolve_workers(explicit: int | None = None) -> int:
     """Explicit argument beats INVERTOR_WORKERS (engine.py:58-65).  On the
-    B200 build the value is validated and recorded; every step is a single
-    device-wide batched launch, so the result does not depend on it."""
+    B200 build it is the GPU count for run_inversion (gpus_for_workers): the
+    schedule is column-sharded over that many GPUs of this process; the
+    result does not depend on it (K is never split)."""
     if explicit is not None:
         if explicit < 1:
             raise ValueError(f"workers must be >= 1, got {explicit}")
@@ -428,6 +429,35 @@ def _last_step(n_steps: int, stop_after_step) -> int:
     return max(1, min(int(stop_after_step), n_steps))
 
 
+def gpus_for_workers(workers: int | None, nblocks: int) -> int:
+    """``workers`` -> GPU count: clamped to the visible GPUs,
+    then the largest power of two that also divides the block count."""
+    if workers is None or workers <= 1:
+        return 1
+    t = _lib.torch()
+    visible = t.cuda.device_count() if t.cuda.is_available() else 1
+    p = 1
+    while p * 2 <= min(workers, visible) and nblocks % (p * 2) == 0:
+        p *= 2
+    return p
+
+
+def _add_counters(counters: OpCounters, sizes, last: int) -> None:
+    """Reference OpCounters of steps 1..last (bi_engine_counters; no device needed)."""
+    L = _lib.lib()
+    h = _lib._vp()
+    arr = (_lib._c_i64 * len(sizes))(*sizes)
+    _lib.check(L.bi_engine_create(_lib.ctypes.byref(h), len(sizes), arr, 1), "bi_engine_create")
+    try:
+        out = (_lib.ctypes.c_double * 6)()
+        _lib.check(L.bi_engine_counters(h, 1, last, out), "bi_engine_counters")
+    finally:
+        L.bi_engine_destroy(h)
+    counters.multiplies += int(out[0])
+    counters.inversions += int(out[1])
+    counters.reductions += int(out[2])
+
+
 def _check_schedule(schedule: str, stop_after_step) -> None:
     if schedule not in SCHEDULES:
         raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}, got {schedule!r}")
@@ -445,7 +475,7 @@ def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backe
     Extension: ``schedule="pivot_a"`` runs the same partition through the 2n^3
     block-level pivot-A recursion (invertor_by_a, recursive.py:83-123) instead
     of the Eq. 7 steps (SURVEY 8f #1); counters then follow invertor_by_a."""
-    resolve_workers(workers)
+    workers = resolve_workers(workers)
     _check_schedule(schedule, stop_after_step)
     if file_backed and checkpoint_dir is None:
         raise ValueError("file-backed mode needs a checkpoint directory")  # storage.py:396-397
@@ -455,6 +485,15 @@ def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backe
             raise ValueError("checkpoints hold Eq. 7 step-boundary state; use schedule='eq7'")
         return _run_checkpointed(scheme, np.ascontiguousarray(dense, dtype=np.float64), checkpoint_dir,
                                  file_backed, stop_after_step, counters)
+    gpus = gpus_for_workers(workers, len(scheme.sizes)) if schedule == "eq7" else 1
+    if gpus > 1:  # column-sharded over this process's GPUs, one thread per GPU
+        from .distributed import run_inversion_local
+
+        out = run_inversion_local(np.ascontiguousarray(dense, dtype=np.float64), list(scheme.sizes), gpus,
+                                  stop_after_step=stop_after_step)
+        if counters is not None:
+            _add_counters(counters, scheme.sizes, _last_step(total_steps(len(scheme.sizes)), stop_after_step))
+        return BlockMatrix(scheme, MemoryBlockStore(scheme, out), role="inverse")
     eng = _engine_for(scheme.sizes, 1, schedule)
     last = _last_step(eng.n_steps, stop_after_step)
     dense = np.ascontiguousarray(dense, dtype=np.float64)

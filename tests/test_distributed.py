@@ -110,3 +110,58 @@ def test_sharded_two_ranks_one_gpu_bitwise():
     single = bi.run_inversion(well_conditioned(n, seed), sizes=sizes).to_dense()
     assert np.array_equal(out[0], single)
     assert np.array_equal(out[1], single)
+
+
+# --- one process, one thread per GPU (run_inversion(workers=P), local_group.py) ---
+
+@pytest.mark.parametrize("gpus,sizes", [(2, [6] * 4), (2, [5, 7, 6, 4, 8, 3, 5, 6]), (4, [8] * 8),
+                                        (4, [2, 7, 5, 3, 6, 4, 9, 1])])
+def test_local_threads_schedule_cpu(gpus, sizes):
+    from paper_2305_11103_b200.distributed import run_inversion_local
+
+    n = sum(sizes)
+    m = well_conditioned(n, 950 + n)
+    out = run_inversion_local(m, sizes, gpus, backend_factory=TorchCPUBackend)
+    ref = oracle.run_inversion(m, sizes=sizes, leaf_inverter=oracle.gauss_jordan)
+    assert np.max(np.abs(out - ref)) <= 1e-12 * n
+
+
+def test_local_threads_failure_does_not_hang():
+    from paper_2305_11103_b200.distributed import run_inversion_local
+
+    class Failing(TorchCPUBackend):
+        def inverse(self, blocks, outs):
+            raise RuntimeError("leaf failure on purpose")
+
+    with pytest.raises(RuntimeError, match="on purpose"):
+        run_inversion_local(well_conditioned(24, 3), [6] * 4, 2, backend_factory=Failing)
+
+
+def test_workers_to_gpu_count(monkeypatch):
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.engine import gpus_for_workers
+
+    t = _lib.torch()
+    monkeypatch.setattr(t.cuda, "is_available", lambda: True)
+    monkeypatch.setattr(t.cuda, "device_count", lambda: 8)
+    assert gpus_for_workers(None, 8) == 1 and gpus_for_workers(1, 8) == 1
+    assert gpus_for_workers(8, 8) == 8 and gpus_for_workers(8, 64) == 8
+    assert gpus_for_workers(6, 8) == 4 and gpus_for_workers(16, 8) == 8
+    assert gpus_for_workers(8, 4) == 4 and gpus_for_workers(8, 2) == 2
+    assert gpus_for_workers(4, 1) == 1  # one diagonal block: nothing to shard
+    monkeypatch.setattr(t.cuda, "device_count", lambda: 2)
+    assert gpus_for_workers(8, 8) == 2
+
+
+@pytest.mark.gpu
+def test_local_threads_two_on_one_gpu_bitwise():
+    """Two threads sharing the B200 run the sharded schedule with peer-copy
+    exchanges: bitwise equal to the single-device engine."""
+    import paper_2305_11103_b200 as bi
+    from paper_2305_11103_b200.distributed import run_inversion_local
+
+    sizes = [64] * 8
+    m = well_conditioned(512, 78)
+    out = run_inversion_local(m, sizes, 2, devices=[0, 0])
+    single = bi.run_inversion(m, sizes=sizes).to_dense()
+    assert np.array_equal(out, single)
