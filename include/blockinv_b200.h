@@ -71,6 +71,14 @@ int bi_inv_batched(int count, int64_t n,
                    double* out, int64_t ld_out, int64_t stride_out,
                    int* info, void* workspace, int64_t workspace_bytes,
                    void* stream);
+/* Same with arbitrary blocks: in[i] / out[i] and their leading dimensions
+ * are DEVICE arrays of `count` entries (the engine's pointer-table form; the
+ * sharded scheduler batches every equal-order leaf of a step this way). */
+int bi_inv_batched_ptrs(int count, int64_t n,
+                        const double* const* in, const int64_t* ld_in,
+                        double* const* out, const int64_t* ld_out,
+                        int* info, void* workspace, int64_t workspace_bytes,
+                        void* stream);
 
 /* ------------------------------------------------------------------------
  * Step engine: run_inversion (engine.py:482-542) over `batch` independent

@@ -33,6 +33,7 @@ SIGNATURES = [
     ("bi_inv_workspace_bytes", _c_i64, [_c_int, _c_i64]),
     ("bi_inv_batched", _c_int, [_c_int, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64,
                                 _vp, _vp, _c_i64, _vp]),
+    ("bi_inv_batched_ptrs", _c_int, [_c_int, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _vp]),
     ("bi_engine_create", _c_int, [ctypes.POINTER(_vp), _c_int, ctypes.POINTER(_c_i64), _c_int]),
     ("bi_engine_create_ex", _c_int, [ctypes.POINTER(_vp), _c_int, ctypes.POINTER(_c_i64), _c_int, _c_int]),
     ("bi_engine_timeline", _c_int, [_vp, ctypes.POINTER(ctypes.c_float)]),

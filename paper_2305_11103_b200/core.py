@@ -80,23 +80,35 @@ def _disjoint(x, y) -> bool:
 
 def device_gemm(a, b, d, c=None, negate=False):
     """K1 on device tensors: d = [c] + (+-1) a @ b.  2-D views with unit
-    column stride; `c` may be `d` (in-place accumulate)."""
-    m, k = a.shape
-    n = b.shape[1]
-    if b.shape[0] != k or tuple(d.shape) != (m, n) or (c is not None and tuple(c.shape) != (m, n)):
+    column stride, or 3-D strided batches ([batch, rows, cols]; a 2-D operand
+    is broadcast over the batch); `c` may be `d` (in-place accumulate)."""
+    batched = d.dim() == 3
+    bsz = d.shape[0] if batched else 1
+
+    def spec(x):
+        if x is None:
+            return None, 0, 0
+        if x.dim() == 3:
+            if not batched or x.shape[0] != bsz:
+                raise DimensionMismatch(f"gemm batch {tuple(x.shape)} vs {tuple(d.shape)}")
+            return _lib.ptr(x), _lib.ld(x), int(x.stride(0))
+        return _lib.ptr(x), _lib.ld(x), 0
+
+    m, k = a.shape[-2:]
+    n = b.shape[-1]
+    if b.shape[-2] != k or tuple(d.shape[-2:]) != (m, n) or (c is not None and tuple(c.shape[-2:]) != (m, n)):
         raise DimensionMismatch(f"gemm {tuple(a.shape)} x {tuple(b.shape)} -> {tuple(d.shape)}")
-    L = _lib.lib()
-    rc = L.bi_gemm(m, n, k, -1 if negate else 1,
-                   _lib.ptr(a), _lib.ld(a), 0, _lib.ptr(b), _lib.ld(b), 0,
-                   _lib.ptr(c) if c is not None else None, _lib.ld(c) if c is not None else 0, 0,
-                   _lib.ptr(d), _lib.ld(d), 0, 1, _lib.stream_ptr())
+    (pa, lda, sa), (pb, ldb, sb), (pc, ldc, sc), (pd, ldd, sd) = spec(a), spec(b), spec(c), spec(d)
+    rc = _lib.lib().bi_gemm(m, n, k, -1 if negate else 1, pa, lda, sa, pb, ldb, sb, pc, ldc if c is not None else 0,
+                            sc, pd, ldd, sd, bsz, _lib.stream_ptr())
     _lib.check(rc, "bi_gemm")
 
 
-def device_inverse(blocks, out):
+def device_inverse(blocks, out, sync: bool = True):
     """K3 on a device batch: out[i] = inverse(blocks[i]).  `blocks`/`out` are
     [count, n, n] (or [n, n]) views with unit column stride.  Returns the
-    per-block info array (numpy): 0 ok, c+1 first singular pivot column."""
+    per-block info array (numpy): 0 ok, c+1 first singular pivot column;
+    ``sync=False`` returns the device info tensor without waiting."""
     t = _lib.torch()
     single = blocks.dim() == 2
     if single:
@@ -111,7 +123,33 @@ def device_inverse(blocks, out):
                           _lib.ptr(out), _lib.ld(out), int(out.stride(0)), _lib.ptr(info),
                           _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
     _lib.check(rc, "bi_inv_batched")
-    return info.cpu().numpy()
+    return info.cpu().numpy() if sync else info
+
+
+def device_inverse_list(blocks, outs):
+    """K3 on arbitrary equal-order device blocks: outs[i] = inverse(blocks[i])
+    for 2-D views anywhere in device memory (pointer-table form,
+    bi_inv_batched_ptrs).  Returns the device info tensor (no host sync)."""
+    t = _lib.torch()
+    count = len(blocks)
+    n = blocks[0].shape[0]
+    for b_, o_ in zip(blocks, outs):
+        if tuple(b_.shape) != (n, n) or tuple(o_.shape) != (n, n):
+            raise DimensionMismatch(f"inverse of {tuple(b_.shape)} into {tuple(o_.shape)} (order {n})")
+    dev = blocks[0].device
+    # page-locked staging: a pageable H2D copy would block the host until the
+    # stream drains, serialising host and device at every call
+    tab_h = t.tensor([[b_.data_ptr() for b_ in blocks], [_lib.ld(b_) for b_ in blocks],
+                      [o_.data_ptr() for o_ in outs], [_lib.ld(o_) for o_ in outs]], dtype=t.int64).pin_memory()
+    tab = tab_h.to(dev, non_blocking=True)
+    L = _lib.lib()
+    ws = _lib.workspace(L.bi_inv_workspace_bytes(count, n))
+    info = t.zeros((count,), dtype=t.int32, device=dev)
+    rc = L.bi_inv_batched_ptrs(count, n, _lib.ptr(tab[0]), _lib.ptr(tab[1]), _lib.ptr(tab[2]), _lib.ptr(tab[3]),
+                               _lib.ptr(info), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "bi_inv_batched_ptrs")
+    info._bi_keepalive = (tab_h, tab, ws)  # staging and tables live until the caller drops the info
+    return info
 
 
 # ---------------------------------------------------------------------------

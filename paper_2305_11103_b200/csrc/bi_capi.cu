@@ -200,6 +200,28 @@ extern "C" int bi_inv_batched(int count, int64_t n, const double* in, int64_t ld
   return 0;
 }
 
+extern "C" int bi_inv_batched_ptrs(int count, int64_t n, const double* const* in, const int64_t* ld_in,
+                                   double* const* out, const int64_t* ld_out, int* info, void* workspace,
+                                   int64_t workspace_bytes, void* stream) {
+  BI_REQUIRE(count >= 0 && n >= 0, "negative dimension");
+  if (count == 0 || n == 0) return 0;
+  BI_REQUIRE(n <= 8192, "block order above 8192 is not supported by the leaf kernel");
+  BI_REQUIRE(in && ld_in && out && ld_out && info && workspace, "null argument");
+  BI_REQUIRE(workspace_bytes >= bi_inv_workspace_bytes(count, n), "workspace too small");
+  BI_CUDA_TRY(init_attributes());
+  InvGroup g{};
+  g.n = (int)n;
+  g.count = count;
+  g.src_ptrs = in;
+  g.src_lds = ld_in;
+  g.dst_ptrs = out;
+  g.dst_lds = ld_out;
+  inv_group_layout(g, workspace);
+  g.info = info;
+  BI_CUDA_TRY(launch_inv_group(g, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // Single-level Schur paths (schur.py:114-164, 219-259)
 // workspace: [Pinv p*p][Qinv q*q][X q*p][Y p*q][S max(p,q)^2][info 8 ints][K3 scratch]

@@ -55,10 +55,64 @@ class DeviceBackend:
         device_gemm(a, b, d, c=c, negate=negate)
 
     def inverse(self, blocks, outs):
-        """blocks/outs: [count, b, b] strided views; returns info (numpy)."""
+        """blocks/outs: [count, b, b] strided views; returns the device info
+        tensor (no host sync; checked after the run)."""
         from .core import device_inverse
 
-        return device_inverse(blocks, outs)
+        return device_inverse(blocks, outs, sync=False)
+
+    def inverse_list(self, blocks, outs):
+        """Equal-order blocks anywhere in device memory, one K3 launch chain
+        (pointer tables); returns the device info tensor."""
+        from .core import device_inverse_list
+
+        return device_inverse_list(blocks, outs)
+
+
+def _batched_gemms(be, products):
+    """products: list of (a, b, d, c, negate) of one kind over the quads of a
+    level, in quad order.  Split in one pass into maximal runs whose windows
+    line up (same storage, shape and strides, constant offset step per
+    operand) and issue one strided-batch launch per run: a whole level when
+    the partition is uniform and the windows share a buffer, one run per
+    covering T-set square otherwise."""
+
+    def key(v):
+        try:
+            store = v.untyped_storage().data_ptr()
+        except (AttributeError, RuntimeError):
+            store = id(v)
+        return (store, tuple(v.shape), tuple(v.stride())), v.storage_offset()
+
+    n = len(products)
+    ops = [[key(p[k]) if p[k] is not None else None for k in range(4)] for p in products]
+    i = 0
+    while i < n:
+        j = i + 1
+        if j < n:
+            ok = all((ops[i][k] is None) == (ops[j][k] is None) for k in range(4))
+            steps = [None if ops[i][k] is None else ops[j][k][1] - ops[i][k][1] for k in range(4)]
+            ok = ok and all(s is None or s > 0 for s in steps)
+            while ok and j < n:
+                for k in range(4):
+                    if ops[i][k] is None:
+                        continue
+                    if ops[j][k][0] != ops[i][k][0] or ops[j][k][1] - ops[j - 1][k][1] != steps[k]:
+                        ok = False
+                        break
+                if ok:
+                    j += 1
+        run = products[i:j]
+        if len(run) == 1:
+            a, b, d, c, neg = run[0]
+            be.gemm(a, b, d, c=c, negate=neg)
+        else:
+            def stack(k):
+                v0 = run[0][k]
+                return v0.as_strided((len(run),) + tuple(v0.shape), (steps[k],) + tuple(v0.stride()),
+                                     v0.storage_offset())
+            be.gemm(stack(0), stack(1), stack(2), c=stack(3) if run[0][3] is not None else None, negate=run[0][4])
+        i = j
 
 
 def _group_ranks(rank: int, group_size: int) -> list[int]:
@@ -96,13 +150,22 @@ class ShardedEngine:
         self.Minv = self.be.empty(self.n, self.w)
         self.T = {}
         for lv in range(1, self.k + 1):
+            shapes = {}
             for g in range(self.nb >> lv):
                 first, last = g << lv, (g + 1) << lv
                 if last <= self.h0 or first >= self.h1:
                     continue
                 side = self.off[last] - self.off[first]
                 cols = self.off[min(last, self.h1)] - self.off[max(first, self.h0)]
-                self.T[(lv, g)] = self.be.empty(side, cols)
+                shapes[g] = (side, cols)
+            if len(set(shapes.values())) == 1:  # equal quads: one stacked buffer (batchable windows)
+                side, cols = next(iter(shapes.values()))
+                buf = self.be.empty(side * len(shapes), cols)
+                for i, g in enumerate(sorted(shapes)):
+                    self.T[(lv, g)] = buf[i * side:(i + 1) * side]
+            else:
+                for g, (side, cols) in shapes.items():
+                    self.T[(lv, g)] = self.be.empty(side, cols)
         # rank groups for the global levels (created collectively, same order everywhere)
         self.groups = {}
         world_ranks = list(range(self.P))
@@ -150,6 +213,15 @@ class ShardedEngine:
     # -- step actions -------------------------------------------------------
     def _diag(self, act, stepid):
         blocks = list(range(self.h0, self.h1))
+        if hasattr(self.be, "inverse_list"):  # every equal-order leaf of the step in one call
+            by_size = {}
+            for p in blocks:
+                by_size.setdefault(self.sizes[p], []).append(p)
+            for b, ps in by_size.items():
+                src = [self.src_win(act, p, p + 1, p, p + 1) for p in ps]
+                dst = [self.minv_win(p, p + 1, p, p + 1) for p in ps]
+                self._infos.append((stepid, ps, self.be.inverse_list(src, dst)))
+            return
         # group runs of equal-size consecutive blocks inside one buffer
         runs, cur = [], [blocks[0]]
         for p in blocks[1:]:
@@ -167,10 +239,7 @@ class ShardedEngine:
             cnt = len(run)
             src = src0.as_strided((cnt, b, b), (b * (src0.stride(0) + 1), src0.stride(0), 1))
             dst = dst0.as_strided((cnt, b, b), (b * (dst0.stride(0) + 1), dst0.stride(0), 1))
-            info = self.be.inverse(src, dst)
-            bad = np.nonzero(np.asarray(info))[0]
-            if len(bad) and self._first_fail is None:
-                self._first_fail = (stepid, run[int(bad[0])])
+            self._infos.append((stepid, run, self.be.inverse(src, dst)))  # resolved in check()
 
     def _quad(self, level, g):
         first = g << level
@@ -214,6 +283,9 @@ class ShardedEngine:
         lv = act.sid
         be = self.be
         if not self.is_global(lv):
+            # all local quads of the level at once: R and L, then S_D and S_A
+            # (one strided-batch launch per product when the quads are equal-sized)
+            r_ops, l_ops, sd_ops, sa_ops = [], [], [], []
             for g in range(self.h0 >> lv, self.h1 >> lv):
                 first, mid, last = self._quad(lv, g)
                 A = self.src_win(act, first, mid, first, mid)
@@ -222,10 +294,12 @@ class ShardedEngine:
                 D = self.src_win(act, mid, last, mid, last)
                 R = self.t_win(lv, first, mid, mid, last)
                 L = self.t_win(lv, mid, last, first, mid)
-                be.gemm(self.minv_win(first, mid, first, mid), B, R, negate=True)
-                be.gemm(self.minv_win(mid, last, mid, last), C, L, negate=True)
-                be.gemm(B, L, self.t_win(lv, first, mid, first, mid), c=A)
-                be.gemm(C, R, self.t_win(lv, mid, last, mid, last), c=D)
+                r_ops.append((self.minv_win(first, mid, first, mid), B, R, None, True))
+                l_ops.append((self.minv_win(mid, last, mid, last), C, L, None, True))
+                sd_ops.append((B, L, self.t_win(lv, first, mid, first, mid), A, False))
+                sa_ops.append((C, R, self.t_win(lv, mid, last, mid, last), D, False))
+            for ops in (r_ops, l_ops, sd_ops, sa_ops):
+                _batched_gemms(be, ops)
             return
         import torch
 
@@ -267,12 +341,15 @@ class ShardedEngine:
     def _updown(self, lv):
         be = self.be
         if not self.is_global(lv):
+            down, up = [], []
             for g in range(self.h0 >> lv, self.h1 >> lv):
                 first, mid, last = self._quad(lv, g)
-                be.gemm(self.t_win(lv, mid, last, first, mid), self.minv_win(first, mid, first, mid),
-                        self.minv_win(mid, last, first, mid))
-                be.gemm(self.t_win(lv, first, mid, mid, last), self.minv_win(mid, last, mid, last),
-                        self.minv_win(first, mid, mid, last))
+                down.append((self.t_win(lv, mid, last, first, mid), self.minv_win(first, mid, first, mid),
+                             self.minv_win(mid, last, first, mid), None, False))
+                up.append((self.t_win(lv, first, mid, mid, last), self.minv_win(mid, last, mid, last),
+                           self.minv_win(first, mid, mid, last), None, False))
+            _batched_gemms(be, down)
+            _batched_gemms(be, up)
             return
         import torch
 
@@ -310,6 +387,7 @@ class ShardedEngine:
         if first == 1:
             self.Minv.zero_()
         self._first_fail = None
+        self._infos = []
         for stepid in range(first, last + 1):
             act = decode_step(loopid_for_step(stepid, self.nb))
             if act.kind == INVERT_DIAGONALS:
@@ -326,6 +404,12 @@ class ShardedEngine:
         rank (engine.py:320-328); collective."""
         import torch
 
+        for stepid, run, info in getattr(self, "_infos", []):
+            info = info.cpu().numpy() if torch.is_tensor(info) else np.asarray(info)
+            bad = np.nonzero(info)[0]
+            if len(bad) and self._first_fail is None:
+                self._first_fail = (stepid, run[int(bad[0])])
+        self._infos = []
         mine = self._first_fail or (1 << 30, 1 << 30)
         t = torch.tensor([mine[0] * (self.nb + 1) + mine[1]], dtype=torch.int64)
         if self.dist.get_backend(self.group) == "nccl":
