@@ -156,3 +156,28 @@ def test_residual_kernel(bi):
     y = x + 1e-6 * g.standard_normal(x.shape)  # a residual far above rounding must match closely
     assert abs(bi.residual_frobenius(m, y) - oracle.residual_frob(m, y)) <= 1e-10 * oracle.residual_frob(m, y)
     assert bi.residual_norm(np.eye(4), np.eye(4)) == 0.0
+
+
+def test_inverse_pointer_table_form(bi):
+    """bi_inv_batched_ptrs: equal-order blocks scattered over different buffers
+    (odd leading dimensions, different source/destination strides) equal the
+    oracle's pivoted GJ, and a singular block is flagged in its slot."""
+    import torch
+
+    from paper_2305_11103_b200.core import device_inverse_list
+
+    n = 48
+    mats = [well_conditioned(n, 300 + i) for i in range(5)]
+    mats[3] = np.ones((n, n))  # singular
+    bufs = [torch.zeros((n + 7, n + 13), dtype=torch.float64, device="cuda") for _ in range(5)]
+    outs_buf = torch.zeros((5 * n + 3, n + 5), dtype=torch.float64, device="cuda")
+    blocks, outs = [], []
+    for i, m in enumerate(mats):
+        v = bufs[i][3:3 + n, 5:5 + n]
+        v.copy_(torch.from_numpy(m))
+        blocks.append(v)
+        outs.append(outs_buf[1 + i * n:1 + (i + 1) * n, 2:2 + n])
+    info = device_inverse_list(blocks, outs).cpu().numpy()
+    assert info[3] != 0 and all(info[i] == 0 for i in (0, 1, 2, 4))
+    for i in (0, 1, 2, 4):
+        assert oracle.rel_frob(outs[i].cpu().numpy(), oracle.gauss_jordan(mats[i])) <= 1e-12
