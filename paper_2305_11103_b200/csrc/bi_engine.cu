@@ -889,6 +889,7 @@ static cudaError_t lane_io_post(bi_engine* e, int lane, cudaStream_t ls, const H
 static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t s, int mask = 3,
                                  const HostIO* io = nullptr) {
   cudaError_t err = cudaSuccess;
+  cudaEvent_t last_h2d = nullptr;  // the copy stream's final piece (joined into `s` at the end)
   e->set_policy(io && io->out ? 1 : 0);
   const bool fork = e->nlanes > 1 || (io && io->in);
   if (e->timeline) err = cudaEventRecordWithFlags(e->tl_start, s, cudaEventRecordExternal);
@@ -932,6 +933,7 @@ static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t
           }
         }
         if (err == cudaSuccess) err = cudaEventRecord(e->ev_h2d[(size_t)z * (e->k + 1) + lv], e->copy_stream);
+        last_h2d = e->ev_h2d[(size_t)z * (e->k + 1) + lv];
       }
     }
   }
@@ -958,6 +960,9 @@ static cudaError_t enqueue_steps(bi_engine* e, int first, int last, cudaStream_t
   }
   for (int l = split ? 0 : 1; l < e->nlanes && err == cudaSuccess; ++l)
     err = cudaStreamWaitEvent(s, e->ev_join[l], 0);
+  // a run that stops early never waits on its later input pieces: join the
+  // copy stream explicitly (graph capture rejects unjoined work)
+  if (err == cudaSuccess && last_h2d) err = cudaStreamWaitEvent(s, last_h2d, 0);
   return err;
 }
 
