@@ -52,6 +52,23 @@ int bi_gemm(int64_t m, int64_t n, int64_t k, int alpha_sign,
             const double* cin, int64_t ldc, int64_t stride_c,
             double* d, int64_t ldd, int64_t stride_d,
             int batch, void* stream);
+/* Grouped form (ragged batches, e.g. the non-uniform partitions of cfg3 and
+ * the default partition): `count` independent GEMM problems in ONE launch,
+ * each a bi_gemm argument set.  Descriptors live in host memory; with more
+ * than 4 of them the table is copied into `workspace`
+ * (bi_gemm_grouped_workspace_bytes(count) bytes; may be NULL up to 4). */
+typedef struct bi_gemm_desc {
+  int64_t m, n, k;
+  int alpha_sign; /* +1 | -1 */
+  const double* a; int64_t lda, stride_a;
+  const double* b; int64_t ldb, stride_b;
+  const double* cin; int64_t ldc, stride_c; /* cin may be NULL */
+  double* d; int64_t ldd, stride_d;
+  int batch;
+} bi_gemm_desc;
+int64_t bi_gemm_grouped_workspace_bytes(int count);
+int bi_gemm_grouped(int count, const bi_gemm_desc* descs, void* workspace, int64_t workspace_bytes,
+                    void* stream);
 
 /* ------------------------------------------------------------------------
  * K2/K3: batched in-place-style Gauss-Jordan inversion with partial pivoting

@@ -170,6 +170,49 @@ extern "C" int bi_gemm(int64_t m, int64_t n, int64_t k, int alpha_sign, const do
   return 0;
 }
 
+extern "C" int64_t bi_gemm_grouped_workspace_bytes(int count) {
+  if (count < 0) return -1;
+  return count <= kGemmInline ? 0 : a256((int64_t)count * (int64_t)sizeof(GemmDesc));
+}
+
+extern "C" int bi_gemm_grouped(int count, const bi_gemm_desc* descs, void* workspace, int64_t workspace_bytes,
+                               void* stream) {
+  BI_REQUIRE(count >= 0, "negative count");
+  if (count == 0) return 0;
+  BI_REQUIRE(descs != nullptr, "null descriptor array");
+  BI_REQUIRE(count <= kGemmInline || (workspace && workspace_bytes >= bi_gemm_grouped_workspace_bytes(count)),
+             "workspace too small for the descriptor table");
+  std::vector<GemmDesc> gs;
+  gs.reserve(count);
+  for (int i = 0; i < count; ++i) {
+    const bi_gemm_desc& x = descs[i];
+    BI_REQUIRE(x.m >= 0 && x.n >= 0 && x.k >= 0 && x.batch >= 0, "negative dimension");
+    BI_REQUIRE(x.m < INT32_MAX && x.n < INT32_MAX && x.k < INT32_MAX, "dimension too large");
+    BI_REQUIRE(x.alpha_sign == 1 || x.alpha_sign == -1, "alpha_sign must be +1 or -1");
+    BI_REQUIRE(x.d != nullptr && (x.k == 0 || (x.a && x.b)), "null operand");
+    BI_REQUIRE(x.lda >= x.k && x.ldb >= x.n && x.ldd >= x.n && (!x.cin || x.ldc >= x.n),
+               "leading dimension too small");
+    GemmDesc g = make_gemm(x.m, x.n, x.k, x.alpha_sign < 0 ? 1 : 0, x.a, x.lda, x.b, x.ldb, x.cin, x.ldc, x.d,
+                           x.ldd);
+    g.batch = x.batch;
+    g.sA = x.stride_a;
+    g.sB = x.stride_b;
+    g.sC = x.stride_c;
+    g.sD = x.stride_d;
+    gs.push_back(g);
+  }
+  BI_CUDA_TRY(init_attributes());
+  finalize_descs(gs.data(), count);
+  GemmDesc* dd = nullptr;
+  if (count > kGemmInline) {
+    dd = static_cast<GemmDesc*>(workspace);
+    BI_CUDA_TRY(cudaMemcpyAsync(dd, gs.data(), gs.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice,
+                                static_cast<cudaStream_t>(stream)));
+  }
+  BI_CUDA_TRY(launch_gemm(gs.data(), dd, count, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 extern "C" int64_t bi_inv_workspace_bytes(int count, int64_t n) {
   if (count < 0 || n < 0) return -1;
   return a256(inv_group_scratch_bytes((int)n, count));

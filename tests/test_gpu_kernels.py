@@ -181,3 +181,45 @@ def test_inverse_pointer_table_form(bi):
     assert info[3] != 0 and all(info[i] == 0 for i in (0, 1, 2, 4))
     for i in (0, 1, 2, 4):
         assert oracle.rel_frob(outs[i].cpu().numpy(), oracle.gauss_jordan(mats[i])) <= 1e-12
+
+
+def test_gemm_grouped_ragged(bi):
+    """bi_gemm_grouped: 6 independent ragged problems (more than the 4 inline
+    descriptors: the table goes through the workspace), negate / accumulate
+    mixed, one launch; each equals NumPy."""
+    import ctypes
+
+    import torch
+
+    from paper_2305_11103_b200 import _lib
+
+    class Desc(ctypes.Structure):
+        _fields_ = [("m", ctypes.c_int64), ("n", ctypes.c_int64), ("k", ctypes.c_int64), ("alpha_sign", ctypes.c_int),
+                    ("a", ctypes.c_void_p), ("lda", ctypes.c_int64), ("stride_a", ctypes.c_int64),
+                    ("b", ctypes.c_void_p), ("ldb", ctypes.c_int64), ("stride_b", ctypes.c_int64),
+                    ("cin", ctypes.c_void_p), ("ldc", ctypes.c_int64), ("stride_c", ctypes.c_int64),
+                    ("d", ctypes.c_void_p), ("ldd", ctypes.c_int64), ("stride_d", ctypes.c_int64),
+                    ("batch", ctypes.c_int)]
+
+    g = np.random.default_rng(11)
+    shapes = [(100, 60, 30), (7, 5, 3), (256, 130, 512), (64, 64, 64), (1, 300, 17), (200, 1, 9)]
+    keep, descs, refs = [], [], []
+    for i, (m, n, k) in enumerate(shapes):
+        a, b, c = g.standard_normal((m, k)), g.standard_normal((k, n)), g.standard_normal((m, n))
+        da, db, dc = _lib.to_device(a), _lib.to_device(b), _lib.to_device(c)
+        neg, acc = i % 2 == 1, i % 3 == 0
+        dd = dc if acc else _lib.empty_matrix(m, n)
+        keep += [da, db, dc, dd]
+        descs.append(Desc(m, n, k, -1 if neg else 1, _lib.ptr(da), _lib.ld(da), 0, _lib.ptr(db), _lib.ld(db), 0,
+                          _lib.ptr(dc) if acc else None, _lib.ld(dc) if acc else 0, 0, _lib.ptr(dd), _lib.ld(dd), 0, 1))
+        refs.append((dd, (c if acc else 0.0) + (-1.0 if neg else 1.0) * (a @ b), a, b))
+    arr = (Desc * len(descs))(*descs)
+    L = _lib.lib()
+    ws_bytes = L.bi_gemm_grouped_workspace_bytes(len(descs))
+    assert ws_bytes > 0
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    rc = L.bi_gemm_grouped(len(descs), ctypes.cast(arr, ctypes.c_void_p), ctypes.c_void_p(ws.data_ptr()), ws_bytes,
+                           _lib.stream_ptr())
+    assert rc == 0, L.bi_last_error()
+    for dd, ref, a, b in refs:
+        assert np.linalg.norm(dd.cpu().numpy() - ref) <= _gemm_tol(a, b, ref, a.shape[1]) * 10
