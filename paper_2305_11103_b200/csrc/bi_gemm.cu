@@ -65,6 +65,7 @@ struct K1Cfg {
   static constexpr int kStageA = TM * kBK * 8;
   static constexpr int kStage = kStageA + kBK * TN * 8;
   static constexpr int kSmem = kStages * kStage + 1024;
+  static constexpr int kMinBlocks = (TM == 128 && TN == 64) ? 2 : 1;  // 128 x 64: two CTAs per SM
 };
 
 __device__ __forceinline__ void cp_async16(uint8_t* smem, const double* gmem, int src_bytes) {
@@ -190,7 +191,8 @@ __device__ __forceinline__ void gemm_tile(const GemmLaunch& L, const int tile, u
 }
 
 template <int TM, int TN>
-__global__ void __launch_bounds__(K1Cfg<TM, TN>::kThreads) gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
+__global__ void __launch_bounds__(K1Cfg<TM, TN>::kThreads, K1Cfg<TM, TN>::kMinBlocks)
+    gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -247,6 +249,10 @@ cudaError_t gemm_init_attributes() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_dmma_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                K1Cfg<64, 64>::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_dmma_kernel<128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               K1Cfg<128, 64>::kSmem);
+    if (e == cudaSuccess) e = set_carveout(gemm_dmma_kernel<128, 64>);
     if (e == cudaSuccess) e = set_carveout(gemm_dmma_kernel<kBM, kBN>);
     if (e == cudaSuccess) e = set_carveout(gemm_dmma_kernel<64, 64>);
     return e;
@@ -272,6 +278,28 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
   GemmLaunch L{};
   L.count = count;
   L.total_tiles = total;
+  static const int cp_tn = [] {  // BI_GEMM_CP_TN: cp.async tile width (64: two CTAs per SM; 128)
+    const char* v = getenv("BI_GEMM_CP_TN");
+    return (v && atoi(v) == 128) ? 128 : 64;
+  }();
+  if (count <= kGemmInline && cp_tn == 64) {  // inline descriptors: re-tile for 128 x 64
+    int t = 0;
+    for (int i = 0; i < count; ++i) {
+      GemmDesc d = h_descs[i];
+      const bool empty = d.M <= 0 || d.N <= 0 || d.batch <= 0;
+      d.tiles_m = empty ? 0 : (d.M + kBM - 1) / kBM;
+      d.tiles_n = empty ? 1 : (d.N + 63) / 64;
+      d.tile_begin = t;
+      t += empty ? 0 : d.tiles_m * d.tiles_n * d.batch;
+      L.inl[i] = d;
+    }
+    L.descs = nullptr;
+    L.total_tiles = t;
+    const int cap2 = g_gemm_grid_cap > 0 ? 2 * g_gemm_grid_cap : 0;
+    const int grid2 = (cap2 > 0 && cap2 < t) ? cap2 : t;
+    return launch_kernel(gemm_dmma_kernel<128, 64>, dim3(grid2), dim3(K1Cfg<128, 64>::kThreads),
+                         (size_t)K1Cfg<128, 64>::kSmem, stream, 1u, L);
+  }
   if (count <= kGemmInline) {
     for (int i = 0; i < count; ++i) L.inl[i] = h_descs[i];
     L.descs = nullptr;
