@@ -79,7 +79,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # BI_LIB: an alternative build of the same library (A/B timing of kernel variants)
+    p = Path(path or os.environ.get("BI_LIB") or LIB_PATH)
     if not p.exists():
         raise NativeUnavailable(
             f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
