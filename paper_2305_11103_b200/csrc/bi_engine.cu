@@ -185,11 +185,13 @@ struct bi_engine {
     int lane_priority[kMaxLanes] = {};
     int leaf_priority = 0;
     int skew = 1;
+    int gemm_cap = 0;
   } pol[2];  // [0] device-resident runs, [1] runs with host read-back
   void set_policy(int i) {
     for (int l = 0; l < kMaxLanes; ++l) lane_priority[l] = pol[i].lane_priority[l];
     leaf_priority = pol[i].leaf_priority;
     skew_mode = pol[i].skew;
+    gemm_cap = pol[i].gemm_cap;
   }
   int zlo[kMaxLanes] = {}, zhi[kMaxLanes] = {};
   int* info = nullptr;
@@ -631,12 +633,12 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   p += align256(e->info_ints * 4);
   BI_CUDA_TRY(init_attributes());
   {
-    // BI_PRIORITY_MODE: 0 none, 1 lane order (lane 0 highest), 2 leaf kernels
-    // above GEMMs (default)
+    // BI_PRIORITY_MODE: 0 none; 1 lane order (lane 0 highest); 2 leaf kernels
+    // above the GEMMs; 3 leaf kernels highest, then the GEMMs of later-starting
+    // lanes; 4 leaf kernels highest, then the GEMMs in lane order.
     // Two scheduling policies (measured, profiles/r01_engine_policies.txt):
-    //  * device-resident runs: leaf kernels at the highest priority, then the
-    //    GEMMs in lane order; lanes start together (mode 4, skew 0) -- best
-    //    step time with the two-CTA K1 (mode 2 / skew 1 before it);
+    //  * device-resident runs: leaf kernels at the highest priority, GEMMs
+    //    equal, lanes start together (mode 2, skew 0);
     //  * runs that read the inverses back to the host: lane 0 highest, lanes
     //    start together (mode 1, skew 0) -- lanes finish staggered, so the
     //    per-lane read-backs (PCIe-bound, ~2.3 ms each at cfg2) overlap compute.
@@ -646,26 +648,33 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
     for (int pol = 0; pol < 2; ++pol) {
-      const int mode = pe ? atoi(pe) : (pol == 0 ? 4 : 1);
+      const int mode = pe ? atoi(pe) : (pol == 0 ? 2 : 1);
       // mode 3: leaf kernels highest, then the GEMMs of later-starting lanes
       for (int l = 0; l < e->nlanes; ++l) {
         int pr = 0;
         if (mode == 1 && e->nlanes > 1) pr = std::min(greatest + l, least);
         if (mode == 3 && e->nlanes > 1) pr = std::min(greatest + 1 + (e->nlanes - 1 - l), least);
+        if (mode == 4 && e->nlanes > 1) pr = std::min(greatest + 1 + l, least);
         e->pol[pol].lane_priority[l] = pr;
       }
-      e->pol[pol].leaf_priority = (mode == 2 || mode == 3) ? greatest : 0;
+      e->pol[pol].leaf_priority = (mode >= 2 && mode <= 4) ? greatest : 0;
       e->pol[pol].skew = sk ? atoi(sk) : 0;
     }
-    e->set_policy(0);
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const char* rs = getenv("BI_RESERVE_SMS");
-    // measured (profiles/r01_engine_overlap.txt): reserving 16 SMs from the
-    // engine GEMMs lets the leaf chains of the other lanes run alongside
-    const int reserve = rs ? atoi(rs) : (e->nlanes > 1 ? 16 : 0);
-    e->gemm_cap = (reserve > 0 && reserve < nsm) ? nsm - reserve : 0;
+    // BI_RESERVE_SMS: SMs kept out of a persistent (grid-capped) engine GEMM.
+    // Device-resident runs: no cap -- one CTA per tile, so SMs free up at
+    // every tile end and the top-priority leaf kernels of other lanes get them
+    // at once instead of waiting out a persistent GEMM (27.4 -> 27.0 ms).
+    // Host read-back runs keep 16 SMs out of a persistent grid (their lanes
+    // run in lane-priority order; e2e 31.2 -> 31.0 ms).
+    for (int pol = 0; pol < 2; ++pol) {
+      const int reserve = rs ? atoi(rs) : (pol == 0 || e->nlanes == 1 ? 0 : 16);
+      e->pol[pol].gemm_cap = (reserve > 0 && reserve < nsm) ? nsm - reserve : 0;
+    }
+    e->set_policy(0);
   }
   if (!e->d2h_stream[0]) {
     for (int l = 0; l < e->nlanes; ++l) {
