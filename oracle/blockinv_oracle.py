@@ -34,6 +34,7 @@ __all__ = [
     "gauss_jordan",
     "invertor_by_a",
     "invertor_inplace_by_a",
+    "invertor_by_ad",
     "invert_via_a",
     "invert_via_d",
     "invert_via_ad",
@@ -424,6 +425,44 @@ def invertor_by_a(x: np.ndarray) -> np.ndarray:
     """recursive.py:72-80: unpivoted recursive pivot-A inverse into new storage."""
     x = np.asarray(x, dtype=np.float64)
     return _by_a(x, [])
+
+
+def _by_ad(x: np.ndarray, out: np.ndarray, path) -> None:
+    """recursive.py:424-449: both diagonal pivots per node (Eq. 7), leaves of
+    order <= 2 by ``invert_small``; the Schur complements are accumulated
+    in place (schur_accumulate = _mm_acc into a copy of A / D)."""
+    n = x.shape[0]
+    if n <= 2:
+        try:
+            out[...] = invert_small(x)
+        except OracleSingular as exc:
+            raise OracleSingular(exc.block, path) from None
+        return
+    p = n // 2
+    q = n - p
+    a, b, c, d = x[:p, :p], x[:p, p:], x[p:, :p], x[p:, p:]
+    ainv, dinv = np.empty((p, p)), np.empty((q, q))
+    _by_ad(a, ainv, path + ["A"])
+    _by_ad(d, dinv, path + ["D"])
+    n_ab, n_dc = np.empty((p, q)), np.empty((q, p))
+    multiply(ainv, b, n_ab, negate=True)
+    multiply(dinv, c, n_dc, negate=True)
+    s_d = a.copy()
+    mm_acc(b, n_dc, s_d)
+    s_a = d.copy()
+    mm_acc(c, n_ab, s_a)
+    _by_ad(s_d, out[:p, :p], path + ["SchurD"])
+    _by_ad(s_a, out[p:, p:], path + ["SchurA"])
+    multiply(n_ab, out[p:, p:], out[:p, p:])
+    multiply(n_dc, out[:p, :p], out[p:, :p])
+
+
+def invertor_by_ad(x: np.ndarray) -> np.ndarray:
+    """recursive.py:366-385: combined-pivot recursion into new storage."""
+    x = np.asarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _by_ad(x, out, [])
+    return out
 
 
 def _inplace_leaf(x: np.ndarray, path) -> None:

@@ -161,7 +161,10 @@ def to_device(a: np.ndarray):
         d = empty_matrix(a.shape[0], a.shape[1])
     else:
         d = empty_matrix(a.shape[1], a.shape[2], batch=a.shape[0])
-    d.copy_(torch().from_numpy(np.ascontiguousarray(a)))
+    a = np.ascontiguousarray(a)
+    if not a.flags.writeable:  # e.g. a BMAT file's buffer; torch.from_numpy wants a writable array
+        a = a.copy()
+    d.copy_(torch().from_numpy(a))
     return d
 
 

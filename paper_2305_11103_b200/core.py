@@ -14,7 +14,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .errors import DimensionMismatch, ScratchTooSmall, SingularBlock, SingularMatrix
+from .checkpoint import load_binary, matrix_from_bytes, matrix_to_bytes, save_binary  # noqa: F401 (core API)
+from .errors import DimensionMismatch, FormatError, ScratchTooSmall, SingularBlock, SingularMatrix
 
 # Alias checks on every call (core.py:31-47); benchmarks switch them off.
 debug_checks = True
@@ -301,3 +302,57 @@ def residual_frobenius(x, x_inv) -> float:
         raise DimensionMismatch(f"residual_frobenius {x.shape} vs {x_inv.shape}")
     fro, _ = _residual_device(_lib.to_device(x), _lib.to_device(x_inv))
     return float(fro[0])
+
+
+# ---------------------------------------------------------------------------
+# matrix files (core.py:415-484): text "rows cols" + rows, or BMAT binary
+# (BMAT codec shared with the checkpoint writer, checkpoint.py)
+# ---------------------------------------------------------------------------
+
+def _validate_loaded(m: np.ndarray) -> np.ndarray:
+    if m.ndim != 2 or m.shape[0] < 1 or m.shape[1] < 1:
+        raise FormatError(f"bad matrix shape {m.shape}")
+    if not np.all(np.isfinite(m)):
+        raise FormatError("matrix contains NaN or Inf entries")
+    return np.ascontiguousarray(m, dtype=np.float64)
+
+
+def save_text(m, path) -> None:
+    """core.py:437-442: header line, then one line per row (repr floats)."""
+    m = as_matrix(m)
+    with open(path, "w") as fh:
+        fh.write(f"{m.shape[0]} {m.shape[1]}\n")
+        for row in m:
+            fh.write(" ".join(repr(float(v)) for v in row) + "\n")
+
+
+def load_text(path) -> np.ndarray:
+    """core.py:445-460."""
+    with open(path) as fh:
+        header = fh.readline().split()
+        if len(header) != 2:
+            raise FormatError("first line must be 'rows cols'")
+        try:
+            rows, cols = int(header[0]), int(header[1])
+        except ValueError as exc:
+            raise FormatError("non-integer dimensions") from exc
+        try:
+            data = np.loadtxt(fh, ndmin=2, dtype=np.float64)
+        except ValueError as exc:
+            raise FormatError(f"bad matrix body: {exc}") from exc
+    if data.shape != (rows, cols):
+        raise FormatError(f"header says {(rows, cols)}, body is {data.shape}")
+    return _validate_loaded(data)
+
+
+def save_matrix(m, path, binary: bool = False) -> None:
+    """core.py:477-478."""
+    (save_binary if binary else save_text)(m, path)
+
+
+def load_matrix(path, binary: bool | None = None) -> np.ndarray:
+    """core.py:481-486: sniff the BMAT magic when ``binary`` is None."""
+    if binary is None:
+        with open(path, "rb") as fh:
+            binary = fh.read(4) == b"BMAT"
+    return (load_binary if binary else load_text)(path)

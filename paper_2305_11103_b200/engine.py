@@ -186,6 +186,44 @@ def fox_block_multiply(a: BlockedView, b: BlockedView, out: BlockedView, workers
             counters.reductions += 1
 
 
+def assemble_updown(level: int, minv, t_sets: dict, workers: int = 1,
+                    counters: OpCounters | None = None) -> None:
+    """One assembly pass ``level`` on its own (engine.py:460-479, the step
+    interpreter's ``updown_pass``, :396-437): for every level-``level`` quad
+    with completed half-width diagonal inverses in ``minv``,
+    M_inv[D rows, A cols] = L . M_inv[A, A] and M_inv[A rows, D cols] =
+    R . M_inv[D, D], L and R taken from ``t_sets[level]``.  ``minv`` is a
+    BlockMatrix or a MemoryBlockStore and is updated in place.  On the device
+    the pass is two K1 products per quad (the reference's per-block-column
+    tasks are one GEMM each here); ``workers`` is accepted for signature
+    parity."""
+    from .core import device_gemm
+
+    store = minv.store if isinstance(minv, BlockMatrix) else minv
+    scheme = store.scheme
+    if level not in t_sets:
+        raise BlockShapeMismatch(f"no provisional set for level {level}")
+    tset = t_sets[level]
+    if not 1 <= level <= scheme.k:
+        raise BlockShapeMismatch(f"level {level} for {scheme.n_blocks} blocks")
+    resolve_workers(workers)
+    off = scheme.offsets
+    quads = []
+    for g in range(scheme.n_blocks >> level):  # load every operand first (MissingProvisionalData)
+        first, mid, last = tset.spans(g)
+        quads.append((off[first], off[mid], off[last], tset.l_block(g), tset.r_block(g)))
+    dm = _lib.to_device(store.data)
+    for a0, a1, a2, lb, rb in quads:
+        device_gemm(_lib.to_device(lb), dm[a0:a1, a0:a1], dm[a1:a2, a0:a1])  # down: L . M_inv[A, A]
+        device_gemm(_lib.to_device(rb), dm[a1:a2, a1:a2], dm[a0:a1, a1:a2])  # up:   R . M_inv[D, D]
+        if counters is not None:
+            counters.multiplies += 2
+    out = dm[:, : scheme.m_n].cpu().numpy()
+    for a0, a1, a2, _, _ in quads:
+        store.data[a1:a2, a0:a1] = out[a1:a2, a0:a1]
+        store.data[a0:a1, a1:a2] = out[a0:a1, a1:a2]
+
+
 # ---------------------------------------------------------------------------
 # the device engine
 # ---------------------------------------------------------------------------

@@ -1,4 +1,4 @@
-"""Recursive pivot-A inversion on the B200 (recursive.py:72-333).
+"""Recursive blockwise inversion on the B200 (recursive.py:72-496).
 
 The reference recurses Eq. 2 down to 2x2 analytic leaves.  On the device the
 same pivot-A recursion (split floor(n/2), six products and two reductions per
@@ -6,6 +6,14 @@ node) stops at ``LEAF_ORDER`` and inverts the leaves with the K3 pivoted
 Gauss-Jordan kernel -- one native call, ``bi_inplace_by_a``, for the whole
 tree.  The counters report the executed tree (nodes, 6 multiplies and 2
 reductions per node, one inversion per leaf).
+
+``invertor_by_ad`` (both diagonal pivots per node, Eq. 7) recurses on device
+tensors: the (A, D) and (S_D, S_A) pairs of a node whose halves are leaves
+are inverted by one batched K3 call, the four products and two Schur
+reductions are K1 launches, and leaf status is checked once at the end (no
+host sync inside the tree).  ``invertor_with_fallback`` keeps the
+reference's per-node A -> D -> B -> C pivot fallback, each node's formula on
+the device.
 """
 
 from __future__ import annotations
@@ -13,8 +21,8 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .core import OpCounters, as_matrix
-from .errors import DimensionMismatch, ScratchTooSmall, SingularBlock
+from .core import OpCounters, as_matrix, device_gemm, device_inverse
+from .errors import AllPivotsSingular, DimensionMismatch, ScratchTooSmall, SingularBlock
 
 LEAF_ORDER = 256  # device leaf order (reference: 2, recursive.py:44)
 
@@ -81,4 +89,154 @@ def invertor_by_a(x, counters: OpCounters | None = None):
         inplace_by_a_device(xd)
         out[...] = xd.cpu().numpy()
     _tree(n, LEAF_ORDER, counters)
+    return out, counters
+
+
+# ---------------------------------------------------------------------------
+# invertor_by_ad (recursive.py:366-449)
+# ---------------------------------------------------------------------------
+
+
+class _AdTree:
+    """Device Eq. 7 recursion state: pending leaf status and the reference's
+    tallies (nodes, 4 multiplies + 2 reductions per node, one inversion per
+    leaf, Schur workspaces pooled per (position, order, side))."""
+
+    def __init__(self, counters: OpCounters, leaf_order: int):
+        self.counters = counters
+        self.leaf_order = leaf_order
+        self.pending = []  # (device info tensor, [paths])
+        self.pool = {}
+
+    def slot(self, start: int, order: int, side: str, like):
+        key = (start, order, side)
+        if key not in self.pool:
+            self.pool[key] = _lib.empty_matrix(order, order)
+            self.counters.schur_scratch += order * order
+        return self.pool[key]
+
+    def leaves(self, pairs):
+        """Invert [(block, out, path)] (all leaves); equal orders share one
+        K3 launch."""
+        by_order = {}
+        for blk, out, path in pairs:
+            by_order.setdefault(int(blk.shape[0]), []).append((blk, out, path))
+        for n, items in by_order.items():
+            if len(items) == 1:
+                blk, out, path = items[0]
+                self.pending.append((device_inverse(blk, out, sync=False), [path]))
+            else:
+                from .core import device_inverse_list
+
+                info = device_inverse_list([b for b, _, _ in items], [o for _, o, _ in items])
+                self.pending.append((info, [p for _, _, p in items]))
+            self.counters.inversions += len(items)
+
+    def pair(self, x1, o1, s1, p1, x2, o2, s2, p2):
+        """Invert two independent blocks (a reference 'pair' stage)."""
+        leaf1, leaf2 = x1.shape[0] <= self.leaf_order, x2.shape[0] <= self.leaf_order
+        if leaf1 and leaf2:
+            self.leaves([(x1, o1, p1), (x2, o2, p2)])
+            return
+        for x, o, st, p, lf in ((x1, o1, s1, p1, leaf1), (x2, o2, s2, p2, leaf2)):
+            if lf:
+                self.leaves([(x, o, p)])
+            else:
+                self.node(x, o, st, p)
+
+    def node(self, x, out, start: int, path):
+        n = int(x.shape[0])
+        if n <= self.leaf_order:
+            self.leaves([(x, out, path)])
+            return
+        self.counters.nodes += 1
+        p, q = n // 2, n - n // 2
+        a, b, c, d = x[:p, :p], x[:p, p:], x[p:, :p], x[p:, p:]
+        a_inv, d_inv = _lib.empty_matrix(p, p), _lib.empty_matrix(q, q)
+        self.pair(a, a_inv, start, path + ["A"], d, d_inv, start + p, path + ["D"])
+        n_ab, n_dc = _lib.empty_matrix(p, q), _lib.empty_matrix(q, p)
+        device_gemm(a_inv, b, n_ab, negate=True)  # -A^-1 B
+        device_gemm(d_inv, c, n_dc, negate=True)  # -D^-1 C
+        s_d = self.slot(start, p, "sd", a)
+        s_d.copy_(a)
+        device_gemm(b, n_dc, s_d, c=s_d)  # S_D = A - B D^-1 C
+        s_a = self.slot(start + p, q, "sa", d)
+        s_a.copy_(d)
+        device_gemm(c, n_ab, s_a, c=s_a)  # S_A = D - C A^-1 B
+        self.pair(s_d, out[:p, :p], start, path + ["SchurD"], s_a, out[p:, p:], start + p, path + ["SchurA"])
+        device_gemm(n_ab, out[p:, p:], out[:p, p:])  # -A^-1 B S_A^-1
+        device_gemm(n_dc, out[:p, :p], out[p:, :p])  # -D^-1 C S_D^-1
+        self.counters.multiplies += 4
+        self.counters.reductions += 2
+
+    def check(self) -> None:
+        """Raise for the first singular leaf in execution order."""
+        for info, paths in self.pending:
+            bad = np.nonzero(info.cpu().numpy())[0]
+            if bad.size:
+                raise SingularBlock("A", path=paths[int(bad[0])])
+
+
+def invertor_by_ad(x, counters: OpCounters | None = None, parallel_pairs: bool = False):
+    """Both diagonal pivots per node (recursive.py:366-385); returns
+    ``(inverse, counters)``.  Pairs are always independent on the device
+    (batched leaves), so ``parallel_pairs`` changes nothing, as in the
+    reference where results are identical either way."""
+    x = _check_square(x)
+    counters = counters if counters is not None else OpCounters()
+    n = x.shape[0]
+    out = np.empty((n, n))
+    if n:
+        tree = _AdTree(counters, LEAF_ORDER)
+        xd = _lib.to_device(x)
+        od = _lib.empty_matrix(n, n)
+        tree.node(xd, od, 0, [])
+        tree.check()
+        out[...] = od.cpu().numpy()
+    return out, counters
+
+
+# ---------------------------------------------------------------------------
+# invertor_with_fallback (recursive.py:470-496)
+# ---------------------------------------------------------------------------
+
+
+def invertor_with_fallback(x, counters: OpCounters | None = None):
+    """Recursive inversion trying pivots A, D, B, C at every node
+    (recursive.py:470-496); returns ``(inverse, counters)``.  Nodes above
+    ``LEAF_ORDER`` run the reference's per-node fallback
+    (schur.invert_with_fallback with this recursion as ``invert_sub``, each
+    product on the device); leaves use the pivoted K3 kernel, which already
+    handles permutation-like blocks."""
+    from .core import invert_small
+    from .schur import invert_with_fallback
+
+    x = _check_square(x)
+    counters = counters if counters is not None else OpCounters()
+
+    def leaf(block, out):
+        dm = _lib.to_device(as_matrix(block))
+        do = _lib.empty_matrix(*dm.shape)
+        if int(device_inverse(dm, do)[0]):
+            raise SingularBlock("A", path=[])
+        out[...] = do.cpu().numpy()
+        counters.inversions += 1
+
+    def sub(block, out):
+        n = block.shape[0]
+        if n <= LEAF_ORDER:
+            if n <= 4:
+                invert_small(block, out, counters)
+            else:
+                leaf(block, out)
+            return
+        counters.nodes += 1
+        try:
+            invert_with_fallback(block, n // 2, out, invert_sub=sub, counters=counters)
+        except AllPivotsSingular:
+            raise SingularBlock("AllPivots", path=[]) from None
+
+    out = np.empty_like(x)
+    if x.shape[0]:
+        sub(x, out)
     return out, counters

@@ -147,6 +147,31 @@ def main():
             g["cfg3s_a11_singular"] = np.array([0])
         except R.core.SingularMatrix if hasattr(R.core, "SingularMatrix") else Exception:
             g["cfg3s_a11_singular"] = np.array([1])
+        # --- invertor_by_ad / invertor_with_fallback (recursive.py:366-496)
+        for order in (8, 17, 64):
+            m = well_conditioned(order, 30 + order)
+            c = R.OpCounters()
+            g[f"by_ad_{order}"], _ = R.invertor_by_ad(m, c)
+        for order in (6, 16):
+            c = R.OpCounters()
+            g[f"fallback_rec_perm{order}"], _ = R.invertor_with_fallback(np.eye(order)[::-1].copy(), c)
+        # --- bench harness (bench.py): generators, CSV text, slope fit; text matrix file bytes
+        import importlib
+
+        RB = importlib.import_module("blockinv.bench")
+        from blockinv.core import save_text
+
+        for kind in RB.KINDS:
+            for order in (1, 5, 12):
+                g[f"gen_{kind}_{order}"] = RB.generate(order, seed=7, kind=kind)
+        recs = [RB.TimingRecord("a", o, 1, 1e-3 * (o / 8.0) ** 2.9 * (1.0 + 0.03 * ((o * 7) % 5)), 1e-13 * o)
+                for o in (8, 16, 32, 64, 128)]
+        fit = RB.fit_slope(recs, 8, 128)
+        g["bench_fit"] = np.array([fit.exponent, fit.stderr, fit.n_points])
+        g["bench_csv"] = np.frombuffer(RB.records_to_csv(recs).encode(), dtype=np.uint8).copy()
+        with tempfile.TemporaryDirectory() as d:
+            save_text(well_conditioned(3, 5), Path(d) / "m.txt")
+            g["text_file_3"] = np.frombuffer((Path(d) / "m.txt").read_bytes(), dtype=np.uint8).copy()
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(g)} arrays)")
 

@@ -104,6 +104,7 @@ def test_recursive_and_gj_vs_golden(order):
     oracle.invertor_inplace_by_a(x)
     assert x.tobytes() == GOLDEN[f"inplace_{order}"].tobytes()
     assert oracle.gauss_jordan(m).tobytes() == GOLDEN[f"gj_{order}"].tobytes()
+    assert oracle.invertor_by_ad(m).tobytes() == GOLDEN[f"by_ad_{order}"].tobytes()
 
 
 @pytest.mark.parametrize("sizes", [[32] * 2, [16] * 4, [8] * 8])
