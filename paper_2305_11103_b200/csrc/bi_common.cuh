@@ -155,6 +155,25 @@ cudaError_t launch_residual(int64_t n, int batch, const double* a, int64_t lda, 
 // the latency-bound leaf inversions so their CTAs win freed SMs from the
 // throughput-bound GEMMs of the other lane.
 extern thread_local int g_launch_priority;
+// Programmatic dependent launch for the calling thread's launches
+// (cudaLaunchAttributeProgrammaticStreamSerialization; 0 = off).  Set around
+// the K3 chain: each kernel's CTAs may be scheduled while its predecessor in
+// the stream still runs and wait in pdl_enter() for its completion, so the
+// chain's next launch holds its SM slots instead of queueing behind the
+// throughput GEMMs of other lanes at every kernel boundary.
+extern thread_local int g_launch_pdl;
+struct PdlScope {
+  int saved;
+  explicit PdlScope(int on) : saved(g_launch_pdl) { g_launch_pdl = on; }
+  ~PdlScope() { g_launch_pdl = saved; }
+};
+// First statement of every kernel that can sit in a PDL chain: wait for the
+// predecessor grid (a no-op when launched without the attribute).
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Let the successor launch: called where a kernel's remaining work is short
+// (panel epilogue, K1 tile epilogue), so the successor's CTAs are being
+// placed during the tail instead of idling on SM slots for the whole run.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 // Upper bound on K1 grid size (0 = one CTA per tile); K1 is persistent over
 // tiles, so a capped launch still covers every tile.
 extern thread_local int g_gemm_grid_cap;
@@ -178,7 +197,7 @@ cudaError_t launch_kernel_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   unsigned na = 0;
   if (cluster > 1 || force_cluster) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
@@ -190,6 +209,11 @@ cudaError_t launch_kernel_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
   if (g_launch_priority != 0) {
     attr[na].id = cudaLaunchAttributePriority;
     attr[na].val.priority = g_launch_priority;
+    ++na;
+  }
+  if (g_launch_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
   cfg.attrs = attr;

@@ -27,6 +27,7 @@
 namespace bi {
 
 thread_local int g_launch_priority = 0;
+thread_local int g_launch_pdl = 0;
 thread_local int g_gemm_grid_cap = 0;
 
 int carveout_percent() {
@@ -193,6 +194,7 @@ __device__ __forceinline__ void gemm_tile(const GemmLaunch& L, const int tile, u
 template <int TM, int TN>
 __global__ void __launch_bounds__(K1Cfg<TM, TN>::kThreads, K1Cfg<TM, TN>::kMinBlocks)
     gemm_dmma_kernel(const __grid_constant__ GemmLaunch L) {
+  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -90,6 +90,7 @@ __device__ __forceinline__ void k1_compute(const uint8_t* stage, const K1Frag& f
 template <int TM = kBM, int TN = kBN>
 __device__ __forceinline__ void k1_epilogue(const GemmDesc& d, int bz, int m0, int n0, int wm, int wn, int fr, int fc,
                                             double (&acc)[4][4][2]) {
+  pdl_trigger();
   const int mrem = d.M - m0, nrem = d.N - n0;
   const double* C = d.C ? d.C + bz * d.sC : nullptr;
   double* D = d.D + bz * d.sD;

@@ -97,6 +97,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 
 template <int kStages>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_constant__ TmaLaunch L) {
+  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -179,6 +180,7 @@ constexpr int refill_smem() { return kStages * RefillCfg<TN>::kStage + 1024; }
 template <int kStages, int TN>
 __global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks)
     gemm_tma_refill_kernel(const __grid_constant__ TmaLaunch L) {
+  pdl_enter();
   using Cfg = RefillCfg<TN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
