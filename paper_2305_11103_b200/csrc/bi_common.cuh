@@ -127,7 +127,8 @@ struct InvGroup {
   // scratch (device), laid out by inv_group_layout
   double* W;        // count * n * ldw
   int64_t ldw;
-  double* tmp;      // count * 128 * ldw
+  double* tmp;      // count * 128 * ldw  (sub-panel pivot rows: the inner updates' B)
+  double* tmpo;     // count * 128 * ldw  (outer-panel pivot rows: the outer updates' B)
   int* perm;        // count * n
   int* flags;       // count * n
   unsigned long long* maxabs;  // count (bit pattern of max|.|)
