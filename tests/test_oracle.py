@@ -191,3 +191,17 @@ def test_flops_engine_matches_survey():
     assert f["arrows"] == 2 * n**3 - 2 * n**2 * b
     assert f["updown"] == n**3 - n**2 * b
     assert f["leaves"] == 2 * n**2 * b
+
+
+@pytest.mark.parametrize("name,order,seed", [("s8x8", 64, 45), ("s6x16", 96, 47), ("def64", 64, 664)])
+def test_lapack_stand_in_pinned_to_reference(name, order, seed):
+    """The full-size stand-in oracle agrees with the reference's own engine
+    outputs (golden) far inside the 1e-9 parity bar."""
+    m = well_conditioned(order, seed)
+    assert oracle.rel_frob(oracle.lapack_inverse(m), GOLDEN[f"engine_{name}"]) <= 1e-13
+
+
+@pytest.mark.parametrize("order", [8, 17, 64])
+def test_lapack_stand_in_vs_reference_gauss_jordan(order):
+    m = well_conditioned(order, 30 + order)
+    assert oracle.rel_frob(oracle.lapack_inverse(m), GOLDEN[f"gj_{order}"]) <= 1e-13
