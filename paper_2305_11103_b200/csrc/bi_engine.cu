@@ -216,6 +216,8 @@ struct bi_engine {
   cudaStream_t copy_stream = nullptr;       // host->device input copies
   cudaStream_t d2h_stream[kMaxLanes] = {};  // per-lane read-back (page-locked output)
   cudaEvent_t ev_d2h_a[kMaxLanes] = {}, ev_d2h_b[kMaxLanes] = {};
+  static constexpr int kOutChunks = 4;  // row chunks of the last top-level pass, each read back at once
+  cudaEvent_t ev_chunk[kMaxLanes][kOutChunks] = {};
   std::vector<cudaEvent_t> ev_h2d;          // per (matrix, level): that level's input blocks copied
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int last_first = 1, last_last = 0;
@@ -239,6 +241,8 @@ struct bi_engine {
       if (d2h_stream[l]) cudaStreamDestroy(d2h_stream[l]);
       if (ev_d2h_a[l]) cudaEventDestroy(ev_d2h_a[l]);
       if (ev_d2h_b[l]) cudaEventDestroy(ev_d2h_b[l]);
+      for (int c = 0; c < kOutChunks; ++c)
+        if (ev_chunk[l][c]) cudaEventDestroy(ev_chunk[l][c]);
     }
     for (cudaEvent_t ev : ev_h2d) cudaEventDestroy(ev);
     if (meta_dev) cudaFree(meta_dev);
@@ -681,6 +685,8 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
       BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->d2h_stream[l], cudaStreamNonBlocking));
       BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_d2h_a[l], cudaEventDisableTiming));
       BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_d2h_b[l], cudaEventDisableTiming));
+      for (int c = 0; c < bi_engine::kOutChunks; ++c)
+        BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_chunk[l][c], cudaEventDisableTiming));
       if (!e->ev_join[l]) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_join[l], cudaEventDisableTiming));
     }
   }
@@ -774,6 +780,9 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
 struct HostIO;
 static cudaError_t copy_top_quads(bi_engine* e, int lane, const HostIO* io, bool diag, cudaStream_t st);
 
+static cudaError_t pass_in_chunks(bi_engine* e, int lane, const GemmLaunchRec& L, const HostIO* io,
+                                  cudaStream_t s);
+
 static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cudaStream_t s, int mask,
                                 cudaEvent_t after_first = nullptr, bool wait_input = false,
                                 const HostIO* split_io = nullptr) {
@@ -819,6 +828,13 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
         if (skip_leaves) continue;
         PriorityScope leaf_prio(e->leaf_priority ? e->leaf_priority : g_launch_priority);
         err = launch_inv_group(e->invs[op.index].g, s);
+      } else if (split_io && stepid == e->nsteps && &op == &step_ops.back() &&
+                 e->launches[op.index].count <= kGemmInline) {
+        // the last top-level pass writes the off-diagonal top quads: run it in
+        // row chunks and read each chunk back as soon as it is written, so
+        // only the last chunk's copy trails the lane's compute
+        GemmCapScope cap(e->gemm_cap);
+        err = pass_in_chunks(e, lane, e->launches[op.index], split_io, s);
       } else {
         GemmCapScope cap(e->gemm_cap);
         const GemmLaunchRec& L = e->launches[op.index];
@@ -852,6 +868,44 @@ struct HostIO {
 // Read-back of the quads of the top level: diag = the two diagonal quads (final
 // before the top-level up/down pass of the last step), else the two
 // off-diagonal quads (final after it).
+// Row-chunked last pass with per-chunk read-back (see enqueue_lane).  Each
+// descriptor's output lies in M_inv; rows [r0, r1) of every descriptor form
+// chunk c, copied to the host rows at the same coordinates.
+static cudaError_t pass_in_chunks(bi_engine* e, int lane, const GemmLaunchRec& L, const HostIO* io,
+                                  cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+  const int C = bi_engine::kOutChunks;
+  for (int c = 0; c < C && err == cudaSuccess; ++c) {
+    GemmDesc d[kGemmInline];
+    int nd = 0;
+    for (int i = 0; i < L.count; ++i) {
+      GemmDesc x = e->descs[L.first + i];
+      const int r0 = (int)((int64_t)x.M * c / C), r1 = (int)((int64_t)x.M * (c + 1) / C);
+      if (r1 <= r0) continue;
+      x.A += (int64_t)r0 * x.lda;
+      if (x.C) x.C += (int64_t)r0 * x.ldc;
+      x.D += (int64_t)r0 * x.ldd;
+      x.M = r1 - r0;
+      d[nd++] = x;
+    }
+    if (nd == 0) continue;
+    finalize_descs(d, nd);
+    err = launch_gemm(d, nullptr, nd, s);
+    if (err == cudaSuccess) err = cudaEventRecord(e->ev_chunk[lane][c], s);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(e->d2h_stream[lane], e->ev_chunk[lane][c], 0);
+    for (int i = 0; i < nd && err == cudaSuccess; ++i)
+      for (int b = 0; b < d[i].batch && err == cudaSuccess; ++b) {
+        const double* dev = d[i].D + (int64_t)b * d[i].sD;
+        const int64_t off = dev - e->Minv;  // inside matrix z's M_inv
+        const int64_t z = off / e->si, rem = off - z * e->si, row = rem / e->ldi, col = rem - row * e->ldi;
+        err = cudaMemcpy2DAsync(io->out + z * io->s_out + row * io->ld_out + col, io->ld_out * 8, dev,
+                                d[i].ldd * 8, (size_t)d[i].N * 8, (size_t)d[i].M, cudaMemcpyDeviceToHost,
+                                e->d2h_stream[lane]);
+      }
+  }
+  return err;
+}
+
 static cudaError_t copy_top_quads(bi_engine* e, int lane, const HostIO* io, bool diag, cudaStream_t st) {
   cudaError_t err = cudaSuccess;
   const int mid = e->nb / 2;
@@ -884,9 +938,12 @@ static cudaError_t lane_io_post(bi_engine* e, int lane, cudaStream_t ls, const H
   cudaError_t err = cudaSuccess;
   if (!io || !io->out) return err;
   if (io->split_out) {  // the off-diagonal top quads, after the lane's last op
+    // (the lane stream is joined through the read-back stream either way)
     err = cudaEventRecord(e->ev_d2h_b[lane], ls);
     if (err == cudaSuccess) err = cudaStreamWaitEvent(e->d2h_stream[lane], e->ev_d2h_b[lane], 0);
-    if (err == cudaSuccess) err = copy_top_quads(e, lane, io, false, e->d2h_stream[lane]);
+    const auto& ops = e->lane_ops[lane][e->nsteps];
+    const bool chunked = !ops.empty() && ops.back().kind == 1 && e->launches[ops.back().index].count <= kGemmInline;
+    if (err == cudaSuccess && !chunked) err = copy_top_quads(e, lane, io, false, e->d2h_stream[lane]);
     return err;
   }
   for (int z = e->zlo[lane]; z < e->zhi[lane] && err == cudaSuccess; ++z)
