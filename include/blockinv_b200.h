@@ -38,6 +38,18 @@ enum {
 int bi_version(void);
 const char* bi_last_error(void);
 
+/* Device setup (SURVEY 8b bi_init/bi_finalize).  bi_init checks that every
+ * listed device is an sm_100 part (BI_EUNSUPPORTED otherwise), sets the
+ * kernels' attributes there (dynamic shared memory, cluster sizes) and
+ * enables peer access between every pair of listed devices that supports it
+ * (the sharded scheduler's NVLink slab exchanges).  Entry points also
+ * initialise lazily, so calling it is optional; the current device is
+ * preserved.  bi_finalize synchronises the listed devices and releases
+ * library-owned helper streams.  The reference's counterpart is the
+ * engine's worker pool (engine.py:257-270). */
+int bi_init(int ndev, const int* dev_ids);
+int bi_finalize(void);
+
 /* ------------------------------------------------------------------------
  * K1: FP64 DMMA GEMM.  D = [Cin] + (alpha_sign)*A*B, strided batched.
  * Replaces core._mm_acc / multiply / schur_accumulate

@@ -27,6 +27,8 @@ _pdbl = ctypes.POINTER(ctypes.c_double)
 SIGNATURES = [
     ("bi_version", _c_int, []),
     ("bi_last_error", ctypes.c_char_p, []),
+    ("bi_init", _c_int, [_c_int, _pint]),
+    ("bi_finalize", _c_int, []),
     ("bi_gemm", _c_int, [_c_i64, _c_i64, _c_i64, _c_int,
                          _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64,
                          _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _c_int, _vp]),
@@ -126,13 +128,32 @@ def torch():
     return _torch
 
 
+_initialised: set = set()
+
+
 def require_device():
-    """Return the current CUDA device; raise NativeUnavailable without one."""
-    load_library()
+    """Return the current CUDA device; raise NativeUnavailable without one.
+    The first use of a device runs ``bi_init`` on it (sm_100 check, kernel
+    attributes)."""
+    L = load_library()
     t = torch()
     if not t.cuda.is_available():
         raise NativeUnavailable("no CUDA device visible: the B200 library has no CPU fallback")
-    return t.device("cuda", t.cuda.current_device())
+    dev = t.cuda.current_device()
+    if dev not in _initialised:
+        ids = (ctypes.c_int * 1)(dev)
+        check(L.bi_init(1, ids), "bi_init")
+        _initialised.add(dev)
+    return t.device("cuda", dev)
+
+
+def init_devices(devices) -> None:
+    """``bi_init`` over several devices: also enables peer access between
+    them (the sharded scheduler's slab exchanges over NVLink)."""
+    devs = [int(d) for d in devices]
+    ids = (ctypes.c_int * len(devs))(*devs)
+    check(load_library().bi_init(len(devs), ids), "bi_init")
+    _initialised.update(devs)
 
 
 def stream_ptr() -> int:

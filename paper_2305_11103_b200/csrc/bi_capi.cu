@@ -3,6 +3,7 @@
 // pivot-A recursion and the K4 residual kernel.
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -147,6 +148,70 @@ static int64_t a256(int64_t v) { return round_up(v, 256); }
 
 extern "C" int bi_version(void) { return 1; }
 extern "C" const char* bi_last_error(void) { return bi::get_error(); }
+
+static std::vector<int> g_init_devices;
+static std::mutex g_init_mu;
+
+extern "C" int bi_init(int ndev, const int* dev_ids) {
+  BI_REQUIRE(ndev >= 1 && dev_ids, "bi_init needs at least one device id");
+  int count = 0, prev = 0;
+  BI_CUDA_TRY(cudaGetDeviceCount(&count));
+  BI_CUDA_TRY(cudaGetDevice(&prev));
+  for (int i = 0; i < ndev; ++i) BI_REQUIRE(dev_ids[i] >= 0 && dev_ids[i] < count, "device id out of range");
+  int rc = 0;
+  for (int i = 0; i < ndev && rc == 0; ++i) {
+    cudaDeviceProp p{};
+    cudaError_t e = cudaGetDeviceProperties(&p, dev_ids[i]);
+    if (e == cudaSuccess && p.major != 10) {
+      set_error("device is not sm_100 (B200): this library is built for sm_100a only");
+      rc = 5;
+      break;
+    }
+    if (e == cudaSuccess) e = cudaSetDevice(dev_ids[i]);
+    if (e == cudaSuccess) e = init_attributes();
+    for (int j = 0; j < ndev && e == cudaSuccess; ++j) {
+      if (dev_ids[j] == dev_ids[i]) continue;
+      int can = 0;
+      e = cudaDeviceCanAccessPeer(&can, dev_ids[i], dev_ids[j]);
+      if (e == cudaSuccess && can) {
+        e = cudaDeviceEnablePeerAccess(dev_ids[j], 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+          e = cudaSuccess;
+        }
+      }
+    }
+    if (e != cudaSuccess) {
+      set_error(cudaGetErrorString(e));
+      rc = 3;
+    }
+  }
+  cudaSetDevice(prev);
+  if (rc == 0) {
+    std::lock_guard<std::mutex> lock(g_init_mu);
+    for (int i = 0; i < ndev; ++i)
+      if (std::find(g_init_devices.begin(), g_init_devices.end(), dev_ids[i]) == g_init_devices.end())
+        g_init_devices.push_back(dev_ids[i]);
+  }
+  return rc;
+}
+
+extern "C" int bi_finalize(void) {
+  std::vector<int> devs;
+  {
+    std::lock_guard<std::mutex> lock(g_init_mu);
+    devs.swap(g_init_devices);
+  }
+  int prev = 0;
+  BI_CUDA_TRY(cudaGetDevice(&prev));
+  for (int d : devs) {
+    BI_CUDA_TRY(cudaSetDevice(d));
+    BI_CUDA_TRY(cudaDeviceSynchronize());
+  }
+  BI_CUDA_TRY(bi::inv_release_helpers());
+  BI_CUDA_TRY(cudaSetDevice(prev));
+  return 0;
+}
 
 extern "C" int bi_gemm(int64_t m, int64_t n, int64_t k, int alpha_sign, const double* a, int64_t lda,
                        int64_t stride_a, const double* b, int64_t ldb, int64_t stride_b, const double* cin,

@@ -143,6 +143,8 @@ void inv_group_launch_counts(const InvGroup& g, int64_t* kernels, int64_t* gemms
 // Full inversion of the group on `stream`: init, load, panels + updates, store.
 cudaError_t launch_inv_group(const InvGroup& g, cudaStream_t stream);
 cudaError_t inv_init_attributes_public();
+// Destroy K3's helper streams/events (the optional lookahead path); safe to call anytime.
+cudaError_t inv_release_helpers();
 
 // ---------------------------------------------------------------------------
 // K4 residual

@@ -451,6 +451,10 @@ def run_inversion_local(m, sizes, gpus: int, stop_after_step=None, devices=None,
     from .local_group import run_threads
 
     m = np.asarray(m, dtype=np.float64)
+    if backend_factory is None:  # peer access between the participating devices (bi_init)
+        from . import _lib
+
+        _lib.init_devices(sorted(set(devices if devices is not None else range(gpus))))
 
     def target(dist, rank):
         be = backend_factory() if backend_factory is not None else None

@@ -127,7 +127,7 @@ def run_threads(size: int, target, devices=None):
 
     def body(r: int) -> None:
         try:
-            if torch.cuda.is_available():
+            if torch.cuda.is_available() and devices[r] is not None:  # None: host-only rank (tests)
                 torch.cuda.set_device(devices[r])
             results[r] = target(world.facade(r), r)
         except BaseException as exc:  # noqa: BLE001 -- surfaced below

@@ -121,7 +121,7 @@ def test_local_threads_schedule_cpu(gpus, sizes):
 
     n = sum(sizes)
     m = well_conditioned(n, 950 + n)
-    out = run_inversion_local(m, sizes, gpus, backend_factory=TorchCPUBackend)
+    out = run_inversion_local(m, sizes, gpus, backend_factory=TorchCPUBackend, devices=[None] * gpus)
     ref = oracle.run_inversion(m, sizes=sizes, leaf_inverter=oracle.gauss_jordan)
     assert np.max(np.abs(out - ref)) <= 1e-12 * n
 
@@ -134,7 +134,7 @@ def test_local_threads_failure_does_not_hang():
             raise RuntimeError("leaf failure on purpose")
 
     with pytest.raises(RuntimeError, match="on purpose"):
-        run_inversion_local(well_conditioned(24, 3), [6] * 4, 2, backend_factory=Failing)
+        run_inversion_local(well_conditioned(24, 3), [6] * 4, 2, backend_factory=Failing, devices=[None] * 2)
 
 
 def test_workers_to_gpu_count(monkeypatch):

@@ -223,3 +223,20 @@ def test_gemm_grouped_ragged(bi):
     assert rc == 0, L.bi_last_error()
     for dd, ref, a, b in refs:
         assert np.linalg.norm(dd.cpu().numpy() - ref) <= _gemm_tol(a, b, ref, a.shape[1]) * 10
+
+
+def test_init_and_finalize(bi):
+    """bi_init / bi_finalize: sm_100 check and setup on a valid
+    device, an argument error on an invalid one, and the library keeps
+    working after a finalize."""
+    import ctypes
+
+    from paper_2305_11103_b200 import _lib
+
+    L = _lib.load_library()
+    assert L.bi_init(1, (ctypes.c_int * 1)(0)) == 0
+    assert L.bi_init(1, (ctypes.c_int * 1)(4096)) == 2
+    assert L.bi_init(0, None) == 2
+    assert L.bi_finalize() == 0
+    m = well_conditioned(64, 3)
+    assert oracle.rel_frob(bi.gauss_jordan_oracle(m), oracle.gauss_jordan(m)) <= 1e-12
