@@ -11,7 +11,7 @@ into 8 diagonal blocks of order 512, inverted by the reference's step engine
   e2e    : the same metric through the public API run_inversion_batch() with
            page-locked host buffers: H2D of the 4 inputs, the inversion, D2H of
            the 4 inverses inside the timed region.
-  roofline: the dominant kernel K1 (gemm_tma_kernel, FP64 tensor pipe): its
+  roofline: the dominant kernel K1 (gemm_tma_refill_kernel<4, 64>, FP64 tensor pipe): its
            algorithmic flops over its own device time (engine GEMM ops run
            alone), against the measured DMMA peak (MEASURED_PEAKS.json has no
            FP64 entry; profiles/r01_fp64_dmma_dfma_microbench.txt).
@@ -364,7 +364,7 @@ def run_gpu_arm(args) -> None:
                     "api": "paper_2305_11103_b200.run_inversion_batch (pinned host buffers)"},
             "roofline": {"bound": "tensor", "achieved": k1_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": k1_tflops / FP64_PEAK_TFLOPS, "traffic": _load_traffic(),
-                         "kernel": "gemm_tma_kernel (K1 TMA feeder, engine GEMM ops)", "peak_source": FP64_PEAK_SOURCE,
+                         "kernel": "gemm_tma_refill_kernel<4, 64> (K1 TMA feeder, engine GEMM ops)", "peak_source": FP64_PEAK_SOURCE,
                          "kernel_ms_per_step": gemm_ms, "kernel_flops_per_step": counters["gemm_flops"],
                          "share_of_step": gemm_ms / ms_step,
                          "leaf_inversion_ms_per_step": leaf_ms,
