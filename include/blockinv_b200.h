@@ -92,6 +92,10 @@ int bi_gemm_grouped(int count, const bi_gemm_desc* descs, void* workspace, int64
  * engine._leaf_invert (engine.py:449-457) and the `invert_sub(block, out)`
  * plugin protocol (schur.py:16-18, 104-111).  info[i] = 0 on success, or
  * c+1 where c is the first pivot column with no usable pivot.
+ * Blocks above order 8192 (one K3 cluster) are inverted by the pivot-A
+ * recursion (recursive.py:83-123) down to leaves of at most 4096 with
+ * partial pivoting inside each leaf; info is then the first failing leaf's
+ * global column + its leaf info.
  * `workspace` must hold bi_inv_workspace_bytes(count, n) bytes.
  * ---------------------------------------------------------------------- */
 int64_t bi_inv_workspace_bytes(int count, int64_t n);

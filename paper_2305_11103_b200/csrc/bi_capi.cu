@@ -288,7 +288,7 @@ extern "C" int bi_inv_batched(int count, int64_t n, const double* in, int64_t ld
                               int64_t workspace_bytes, void* stream) {
   BI_REQUIRE(count >= 0 && n >= 0, "negative dimension");
   if (count == 0 || n == 0) return 0;
-  BI_REQUIRE(n <= 8192, "block order above 8192 is not supported by the leaf kernel");
+  BI_REQUIRE(n <= INT32_MAX / 2, "block order too large");
   BI_REQUIRE(in && out && info && workspace, "null argument");
   BI_REQUIRE(ld_in >= n && ld_out >= n, "leading dimension too small");
   BI_REQUIRE(workspace_bytes >= bi_inv_workspace_bytes(count, n), "workspace too small");
@@ -313,7 +313,7 @@ extern "C" int bi_inv_batched_ptrs(int count, int64_t n, const double* const* in
                                    int64_t workspace_bytes, void* stream) {
   BI_REQUIRE(count >= 0 && n >= 0, "negative dimension");
   if (count == 0 || n == 0) return 0;
-  BI_REQUIRE(n <= 8192, "block order above 8192 is not supported by the leaf kernel");
+  BI_REQUIRE(n <= INT32_MAX / 2, "block order too large");
   BI_REQUIRE(in && ld_in && out && ld_out && info && workspace, "null argument");
   BI_REQUIRE(workspace_bytes >= bi_inv_workspace_bytes(count, n), "workspace too small");
   BI_CUDA_TRY(init_attributes());
@@ -326,6 +326,21 @@ extern "C" int bi_inv_batched_ptrs(int count, int64_t n, const double* const* in
   g.dst_lds = ld_out;
   inv_group_layout(g, workspace);
   g.info = info;
+  std::vector<const double*> hs(count);
+  std::vector<double*> hd(count);
+  std::vector<int64_t> hsl(count), hdl(count);
+  if (n > kInvMaxDirect) {  // the recursion addresses the blocks from the host: mirror the tables
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    BI_CUDA_TRY(cudaMemcpyAsync(hs.data(), in, count * sizeof(void*), cudaMemcpyDeviceToHost, st));
+    BI_CUDA_TRY(cudaMemcpyAsync(hd.data(), out, count * sizeof(void*), cudaMemcpyDeviceToHost, st));
+    BI_CUDA_TRY(cudaMemcpyAsync(hsl.data(), ld_in, count * 8, cudaMemcpyDeviceToHost, st));
+    BI_CUDA_TRY(cudaMemcpyAsync(hdl.data(), ld_out, count * 8, cudaMemcpyDeviceToHost, st));
+    BI_CUDA_TRY(cudaStreamSynchronize(st));
+    g.h_src_ptrs = hs.data();
+    g.h_src_lds = hsl.data();
+    g.h_dst_ptrs = hd.data();
+    g.h_dst_lds = hdl.data();
+  }
   BI_CUDA_TRY(launch_inv_group(g, static_cast<cudaStream_t>(stream)));
   return 0;
 }
@@ -349,7 +364,6 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
   BI_REQUIRE(m && out && workspace, "null argument");
   BI_REQUIRE(ldm >= n && ldo >= n, "leading dimension too small");
   BI_REQUIRE(workspace_bytes >= bi_schur2x2_workspace_bytes(n, p), "workspace too small");
-  BI_REQUIRE(std::max(p, n - p) <= 8192, "pivot blocks above order 8192 are not supported");
   BI_CUDA_TRY(init_attributes());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t q = n - p, mx = std::max(p, q);

@@ -133,7 +133,18 @@ struct InvGroup {
   int* flags;       // count * n
   unsigned long long* maxabs;  // count (bit pattern of max|.|)
   int* info;        // count (device; caller-visible)
+  // blocks above 8192 (pivot-A recursion with K3 leaves, launch_inv_group):
+  // host mirrors of pointer tables (required with src_ptrs / dst_ptrs) and scratch
+  const double* const* h_src_ptrs;
+  const int64_t* h_src_lds;
+  double* const* h_dst_ptrs;
+  const int64_t* h_dst_lds;
+  double* big_tmp;         // (n - n/2)^2 doubles
+  void* big_leaf_scratch;  // K3 scratch for one leaf
+  int* big_info;           // leaf status slots
 };
+// Largest order the K3 panel kernels take directly (one cluster of 16 x 512 rows).
+constexpr int kInvMaxDirect = 8192;
 
 int64_t inv_group_scratch_bytes(int n, int count);
 // Assign scratch pointers from `base` (needs inv_group_scratch_bytes bytes).

@@ -133,6 +133,11 @@ struct InvRec {
   int info_offset;      // into the info region (ints)
   int lane;             // which lane (scratch region / stream)
   bool in_place = false;  // pivot-A: leaf inverted in place inside M_inv
+  // host mirrors of the pointer tables (blocks above kInvMaxDirect run a host-driven recursion)
+  std::vector<const double*> h_src;
+  std::vector<int64_t> h_srcld;
+  std::vector<double*> h_dst;
+  std::vector<int64_t> h_dstld;
 };
 
 struct Window {
@@ -308,7 +313,7 @@ extern "C" int bi_engine_create_ex(bi_engine** out, int nblocks, const int64_t* 
     e->off.push_back(e->off.back() + sizes[i]);
     maxb = std::max(maxb, sizes[i]);
   }
-  BI_REQUIRE(maxb <= 8192, "diagonal blocks above order 8192 are not supported by the leaf kernel");
+  (void)maxb;  // blocks above kInvMaxDirect invert by a pivot-A recursion with K3 leaves
   e->n = e->off.back();
   // T-set layout (per matrix)
   e->tsq.resize(e->k + 1);
@@ -762,6 +767,14 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
       dst[it] = d.p;
       dstld[it] = d.ld;
     }
+    r.h_src.assign(src, src + r.g.count);
+    r.h_srcld.assign(srcld, srcld + r.g.count);
+    r.h_dst.assign(dst, dst + r.g.count);
+    r.h_dstld.assign(dstld, dstld + r.g.count);
+    r.g.h_src_ptrs = r.h_src.data();
+    r.g.h_src_lds = r.h_srcld.data();
+    r.g.h_dst_ptrs = r.h_dst.data();
+    r.g.h_dst_lds = r.h_dstld.data();
     r.g.src_ptrs = reinterpret_cast<const double* const*>(meta + tabs[i].src);
     r.g.src_lds = reinterpret_cast<const int64_t*>(meta + tabs[i].srcld);
     r.g.dst_ptrs = reinterpret_cast<double* const*>(meta + tabs[i].dst);

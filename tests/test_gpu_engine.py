@@ -404,3 +404,42 @@ def test_batch_wider_than_the_lanes(bi):
     eng.run()
     eng.check()
     assert np.array_equal(eng.Minv[:, :, :128].cpu().numpy(), single)
+
+
+def test_blocks_above_the_k3_limit(bi):
+    """Blocks above 8192 (one K3 cluster) invert by the pivot-A recursion with
+    K3 leaves (launch_inv_group), in the batched leaf API, the pointer-table
+    form, the engine (2 x 9000) and a Schur formula with a 9000 pivot block;
+    checked by device residuals, a singular big block reports its column."""
+    import torch
+
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.core import _residual_device, device_inverse, device_inverse_list
+
+    n = 9000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9000)
+    a = torch.randn((2, n, n), generator=g, dtype=torch.float64, device="cuda") / np.sqrt(n)
+    a[0].diagonal().add_(2.0)
+    a[1].diagonal().add_(3.0)
+    x = _lib.empty_matrix(n, n, batch=2)
+    info = device_inverse(a, x)
+    assert (info == 0).all()
+    fro, mx = _residual_device(a, x, batch=True)
+    assert (fro <= 1e-9 * n).all() and (mx <= 1e-10).all()
+    y = torch.empty_like(a[1])
+    info2 = device_inverse_list([a[1]], [y]).cpu().numpy()
+    assert info2[0] == 0 and torch.equal(y, x[1])
+    s = a[0].clone()
+    s[5000] = 0.0  # a zero row: singular, found in the recursion's second leaf
+    info3 = device_inverse(s, torch.empty_like(s))
+    assert info3[0] != 0
+    # the engine with two 9000-blocks (n = 18000) and Eq. 3 with a 9000 pivot block
+    m = torch.randn((18000, 18000), generator=g, dtype=torch.float64, device="cuda") / np.sqrt(18000.0)
+    m.diagonal().add_(2.0)
+    mh = m.cpu().numpy()
+    inv = bi.run_inversion(mh, sizes=[9000, 9000]).to_dense()
+    assert bi.residual_frobenius(mh, inv) <= 1e-9 * 18000
+    out = np.empty_like(mh)
+    bi.invert_via_d(bi.diagonal_quad(mh, 9000), None, out)
+    assert bi.residual_frobenius(mh, out) <= 1e-9 * 18000
