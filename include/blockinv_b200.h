@@ -81,6 +81,20 @@ typedef struct bi_gemm_desc {
 int64_t bi_gemm_grouped_workspace_bytes(int count);
 int bi_gemm_grouped(int count, const bi_gemm_desc* descs, void* workspace, int64_t workspace_bytes,
                     void* stream);
+/* K1P: all-gather fused into K1 for the sharded scheduler's global levels.
+ * D = [Cin] + (alpha_sign) * [A_0 | ... | A_{nseg-1}] * B, where segment s is
+ * an m x k_segs[s] matrix at a_segs[s] (leading dimension lda_segs[s]) that
+ * may live in a PEER GPU's memory (peer access enabled, e.g. by bi_init):
+ * every k-tile is read from its owner over NVLink while earlier k-tiles are
+ * multiplied, instead of all-gathering the slabs into one buffer first.
+ * Replaces the exchange + multiply of the reference's Fox broadcast step
+ * (engine.fox_block_multiply, engine.py:202-249) across GPUs.  1 <= nseg <= 8;
+ * every segment but the last must be a multiple of 16 columns wide (k-tile
+ * boundaries), so the result is bitwise equal to bi_gemm on the gathered A.
+ * B, Cin and D are local; Cin may equal D. */
+int bi_gemm_kseg(int64_t m, int64_t n, int alpha_sign, int nseg, const double* const* a_segs,
+                 const int64_t* lda_segs, const int64_t* k_segs, const double* b, int64_t ldb,
+                 const double* cin, int64_t ldc, double* d, int64_t ldd, void* stream);
 
 /* ------------------------------------------------------------------------
  * K2/K3: batched in-place-style Gauss-Jordan inversion with partial pivoting

@@ -34,6 +34,8 @@ SIGNATURES = [
                          _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _c_int, _vp]),
     ("bi_gemm_grouped_workspace_bytes", _c_i64, [_c_int]),
     ("bi_gemm_grouped", _c_int, [_c_int, _vp, _vp, _c_i64, _vp]),
+    ("bi_gemm_kseg", _c_int, [_c_i64, _c_i64, _c_int, _c_int, _vp, _vp, _vp,
+                              _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp]),
     ("bi_inv_workspace_bytes", _c_i64, [_c_int, _c_i64]),
     ("bi_inv_batched", _c_int, [_c_int, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64,
                                 _vp, _vp, _c_i64, _vp]),

@@ -105,6 +105,29 @@ def device_gemm(a, b, d, c=None, negate=False):
     _lib.check(rc, "bi_gemm")
 
 
+def device_gemm_kseg(segs, b, d, c=None, negate=False):
+    """K1P: d = [c] + (+-1) [segs[0] | segs[1] | ...] @ b, reading each 2-D
+    segment where it lives (peer GPUs included) instead of gathering it first
+    (bi_gemm_kseg).  Every segment but the last must be a multiple of 16
+    columns wide; the result is bitwise equal to ``device_gemm`` on the
+    concatenation."""
+    import ctypes
+
+    m, n = d.shape
+    widths = [int(s.shape[1]) for s in segs]
+    if any(int(s.shape[0]) != m for s in segs) or b.shape[0] != sum(widths) or b.shape[1] != n \
+            or (c is not None and tuple(c.shape) != (m, n)):
+        raise DimensionMismatch(f"gemm_kseg {[tuple(s.shape) for s in segs]} x {tuple(b.shape)} -> {tuple(d.shape)}")
+    ns = len(segs)
+    ptrs = (ctypes.c_void_p * ns)(*[_lib.ptr(s) for s in segs])
+    lds = (ctypes.c_int64 * ns)(*[_lib.ld(s) for s in segs])
+    ks = (ctypes.c_int64 * ns)(*widths)
+    rc = _lib.lib().bi_gemm_kseg(m, n, -1 if negate else 1, ns, ptrs, lds, ks, _lib.ptr(b), _lib.ld(b),
+                                 _lib.ptr(c) if c is not None else None, _lib.ld(c) if c is not None else 0,
+                                 _lib.ptr(d), _lib.ld(d), _lib.stream_ptr())
+    _lib.check(rc, "bi_gemm_kseg")
+
+
 def device_inverse(blocks, out, sync: bool = True):
     """K3 on a device batch: out[i] = inverse(blocks[i]).  `blocks`/`out` are
     [count, n, n] (or [n, n]) views with unit column stride.  Returns the

@@ -235,6 +235,36 @@ extern "C" int bi_gemm(int64_t m, int64_t n, int64_t k, int alpha_sign, const do
   return 0;
 }
 
+extern "C" int bi_gemm_kseg(int64_t m, int64_t n, int alpha_sign, int nseg, const double* const* a_segs,
+                            const int64_t* lda_segs, const int64_t* k_segs, const double* b, int64_t ldb,
+                            const double* cin, int64_t ldc, double* d, int64_t ldd, void* stream) {
+  BI_REQUIRE(m >= 0 && n >= 0 && m < INT32_MAX && n < INT32_MAX, "bad dimension");
+  BI_REQUIRE(alpha_sign == 1 || alpha_sign == -1, "alpha_sign must be +1 or -1");
+  BI_REQUIRE(nseg >= 1 && nseg <= kMaxKSeg, "nseg must be in [1, 8]");
+  BI_REQUIRE(a_segs && lda_segs && k_segs, "null segment table");
+  int64_t k = 0;
+  for (int s = 0; s < nseg; ++s) {
+    BI_REQUIRE(k_segs[s] >= 0, "negative segment width");
+    BI_REQUIRE(k % kBK == 0, "every segment but the last must be a multiple of 16 wide");
+    BI_REQUIRE(k_segs[s] == 0 || (a_segs[s] && lda_segs[s] >= k_segs[s]), "bad segment operand");
+    k += k_segs[s];
+  }
+  BI_REQUIRE(k < INT32_MAX, "dimension too large");
+  if (m == 0 || n == 0) return 0;
+  BI_REQUIRE(d != nullptr && (k == 0 || b), "null operand");
+  BI_REQUIRE(ldb >= n && ldd >= n && (!cin || ldc >= n), "leading dimension too small");
+  BI_CUDA_TRY(init_attributes());
+  GemmDesc g = make_gemm(m, n, k, alpha_sign < 0 ? 1 : 0, nullptr, 0, b, ldb, cin, ldc, d, ldd);
+  if (k == 0) {  // D = [C]: route through K1 (zero k-tiles, same epilogue)
+    g.A = b;
+    finalize_descs(&g, 1);
+    BI_CUDA_TRY(launch_gemm(&g, nullptr, 1, static_cast<cudaStream_t>(stream)));
+    return 0;
+  }
+  BI_CUDA_TRY(launch_gemm_kseg(g, nseg, a_segs, lda_segs, k_segs, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 extern "C" int64_t bi_gemm_grouped_workspace_bytes(int count) {
   if (count < 0) return -1;
   return count <= kGemmInline ? 0 : a256((int64_t)count * (int64_t)sizeof(GemmDesc));

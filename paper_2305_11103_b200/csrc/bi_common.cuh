@@ -81,6 +81,10 @@ cudaError_t launch_gemm(const GemmDesc* h_descs, const GemmDesc* d_descs, int co
                         cudaStream_t stream);
 // One descriptor on 64 x 64 tiles (latency path; same summation order).
 cudaError_t launch_gemm_small(const GemmDesc& h, cudaStream_t stream);
+// K1P (bi_gemm_peer.cu): A gathered along K from up to kMaxKSeg owners (peer memory).
+constexpr int kMaxKSeg = 8;
+cudaError_t launch_gemm_kseg(const GemmDesc& d, int nseg, const double* const* a, const int64_t* lda,
+                             const int64_t* kseg, cudaStream_t stream);
 
 // Run `fn` once per CUDA device and cache its status: kernel attributes
 // (dynamic shared memory limits, carveouts, cluster permissions) are per

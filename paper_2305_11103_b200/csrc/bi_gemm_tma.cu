@@ -40,6 +40,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -253,6 +254,213 @@ __global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks
   }
 }
 
+// K1P on TMA: the refill ring above with a single descriptor whose A operand
+// is K-segmented over up to kMaxKSeg owners (one tensor map each; a map may
+// describe a peer GPU's memory -- TMA reads it over NVLink).  Segment
+// boundaries lie on k-tiles, so every stage is filled from one owner and the
+// summation order is K1's (bitwise equal to bi_gemm on the gathered A).
+struct alignas(64) TmaSegLaunch {
+  CUtensorMap ta[kMaxKSeg];
+  CUtensorMap tb;
+  GemmDesc d;
+  int kt0[kMaxKSeg];
+  int nseg, tiles_n, total_tiles;
+};
+
+template <int kStages, int TN>
+__global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks)
+    gemm_tma_kseg_kernel(const __grid_constant__ TmaSegLaunch L) {
+  pdl_enter();
+  using Cfg = RefillCfg<TN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ unsigned released[kStages];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / (TN / 32), wn = warp % (TN / 32);
+  const int fr = lane >> 2, fc = lane & 3;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  K1Frag f;
+  k1_frag_init(f, fr, fc);
+  const GemmDesc& d = L.d;
+  const int KT = (d.K + kBK - 1) / kBK;
+
+  // fill `stage` with k-tile `ahead` of `tile` (or of a later tile of this CTA)
+  auto fill = [&](int stage, int tile, int ahead) {
+    tile += (ahead / KT) * gridDim.x;
+    ahead %= KT;
+    if (tile >= L.total_tiles) return;
+    int s = 0;
+    while (s + 1 < L.nseg && L.kt0[s + 1] <= ahead) ++s;
+    const int m0 = (tile / L.tiles_n) * kBM, n0 = (tile % L.tiles_n) * TN;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before async writes
+    uint8_t* sa = smem + stage * Cfg::kStage;
+    uint8_t* sb = sa + kStageA;
+    mbar_expect_tx(&full[stage], Cfg::kStage);
+    tma_load_3d(sa, &L.ta[s], &full[stage], (ahead - L.kt0[s]) * kBK, m0, 0);
+#pragma unroll
+    for (int j = 0; j < TN / 16; ++j) tma_load_3d(sb + j * kBoxBBytes, &L.tb, &full[stage], n0 + 16 * j, ahead * kBK, 0);
+  };
+  if (tid == 0 && (int)blockIdx.x < L.total_tiles)
+    for (int s = 0; s < kStages; ++s) fill(s, blockIdx.x, s);
+
+  unsigned cons_it = 0;
+  for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int stage = cons_it % kStages;
+      mbar_wait(&full[stage], (cons_it / kStages) & 1);
+      k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
+      __syncwarp();
+      if (lane == 0 && atomicAdd(&released[stage], 1u) == Cfg::kWarpsT - 1) {
+        released[stage] = 0;
+        fill(stage, tile, kt + kStages);
+      }
+      ++cons_it;
+    }
+    k1_epilogue<kBM, TN>(d, 0, (tile / L.tiles_n) * kBM, (tile % L.tiles_n) * TN, wm, wn, fr, fc, acc);
+  }
+}
+
+// K1P with TMA multicast across a thread-block cluster of CS CTAs that share
+// one A row block (consecutive 64-column tiles): each CTA loads 128/CS rows of
+// the A k-tile and multicasts them into every CTA of the cluster, so each A
+// element -- a peer's slab, read over NVLink -- is fetched once per cluster
+// instead of once per column tile (remote reads are not cached in the reading
+// GPU's L2; at the K1 rate one column tile per A fetch needs ~2 TB/s, with
+// CS = 4 about 0.5 TB/s, under one NVLink 5 direction).  A stage is refilled
+// only when every CTA of the cluster released it: each CTA's last releasing
+// warp arrives on the `empty` barrier of every cluster CTA, then waits on its
+// own.  Same stage layout, k order and epilogue as K1: bitwise equal.
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, unsigned cta) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                               unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+
+template <int kStages, int CS>
+__global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks)
+    gemm_tma_kseg_mc_kernel(const __grid_constant__ TmaSegLaunch L) {
+  pdl_enter();
+  constexpr int TN = 64;
+  constexpr int kSlice = kBM / CS;  // A rows each CTA loads and multicasts
+  using Cfg = RefillCfg<TN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ unsigned released[kStages];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / (TN / 32), wn = warp % (TN / 32);
+  const int fr = lane >> 2, fc = lane & 3;
+  const unsigned crank = cluster_ctarank();
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CS);
+      released[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  cluster_sync_all();  // every CTA's barriers exist before any remote arrive or multicast
+
+  K1Frag f;
+  k1_frag_init(f, fr, fc);
+  const GemmDesc& d = L.d;
+  const int KT = (d.K + kBK - 1) / kBK;
+  const int groups_n = (L.tiles_n + CS - 1) / CS;
+  const int total_ct = ((d.M + kBM - 1) / kBM) * groups_n;
+  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+  const unsigned short mask = (unsigned short)((1u << CS) - 1);
+
+  auto fill = [&](int stage, int ct, int ahead) {
+    ct += (ahead / KT) * ncl;
+    ahead %= KT;
+    if (ct >= total_ct) return;
+    int s = 0;
+    while (s + 1 < L.nseg && L.kt0[s + 1] <= ahead) ++s;
+    const int m0 = (ct / groups_n) * kBM, n0 = ((ct % groups_n) * CS + (int)crank) * TN;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    uint8_t* sa = smem + stage * Cfg::kStage;
+    uint8_t* sb = sa + kStageA;
+    mbar_expect_tx(&full[stage], Cfg::kStage);  // all CS A slices + this CTA's B boxes
+    tma_load_3d_mc(sa + crank * kSlice * 128, &L.ta[s], &full[stage], (ahead - L.kt0[s]) * kBK, m0 + crank * kSlice, 0,
+                   mask);
+#pragma unroll
+    for (int j = 0; j < TN / 16; ++j) tma_load_3d(sb + j * kBoxBBytes, &L.tb, &full[stage], n0 + 16 * j, ahead * kBK, 0);
+  };
+  if (tid == 0 && cid < total_ct)
+    for (int s = 0; s < kStages; ++s) fill(s, cid, s);
+
+  unsigned cons_it = 0;
+  for (int ct = cid; ct < total_ct; ct += ncl) {
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int stage = cons_it % kStages;
+      mbar_wait(&full[stage], (cons_it / kStages) & 1);
+      k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
+      __syncwarp();
+      if (lane == 0 && atomicAdd(&released[stage], 1u) == Cfg::kWarpsT - 1) {
+        released[stage] = 0;
+        if (ct + ((kt + kStages) / KT) * ncl < total_ct) {  // a refill follows (same test in every CTA)
+          for (int r = 0; r < CS; ++r) mbar_arrive_remote(&empty[stage], r);
+          mbar_wait_cluster(&empty[stage], (cons_it / kStages) & 1);
+          fill(stage, ct, kt + kStages);
+        }
+      }
+      ++cons_it;
+    }
+    const int m0 = (ct / groups_n) * kBM, n0 = ((ct % groups_n) * CS + (int)crank) * TN;
+    k1_epilogue<kBM, TN>(d, 0, m0, n0, wm, wn, fr, fc, acc);  // n0 >= N (cluster padding): stores nothing
+  }
+  cluster_sync_all();  // no CTA exits while a peer may still arrive on its barriers
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_tma_once;
 cudaError_t g_tma_err = cudaSuccess;
@@ -279,6 +487,19 @@ cudaError_t tma_init() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_tma_refill_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                refill_smem<4, 64>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_tma_kseg_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               refill_smem<4, 64>());
+    if (e == cudaSuccess) e = set_carveout(gemm_tma_kseg_kernel<4, 64>);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_tma_kseg_mc_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               refill_smem<4, 64>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_tma_kseg_mc_kernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               refill_smem<4, 64>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_tma_kseg_mc_kernel<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               refill_smem<4, 64>());
     if (e == cudaSuccess) e = set_carveout(gemm_tma_kernel<5>);
     if (e == cudaSuccess) e = set_carveout(gemm_tma_refill_kernel<5, 128>);
     if (e == cudaSuccess) e = set_carveout(gemm_tma_refill_kernel<4, 64>);
@@ -299,6 +520,53 @@ bool encode_3d(CUtensorMap* map, const double* base, uint64_t inner, uint64_t ou
 }
 
 }  // namespace
+
+// K1P on TMA; false when the operands do not qualify (16-byte aligned bases,
+// even leading dimensions) and the caller takes the cp.async K1P kernel.
+bool launch_gemm_kseg_tma(const GemmDesc& d, int nseg, const double* const* a, const int64_t* lda,
+                          const int64_t* kseg, int grid_cap, cudaStream_t stream, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (nseg < 1 || nseg > kMaxKSeg || d.K <= 0 || tma_init() != cudaSuccess) return false;
+  if ((((uintptr_t)d.B) & 15) || (d.ldb & 1)) return false;
+  // BI_KSEG_CLUSTER: CTAs per cluster sharing A by TMA multicast (1: no cluster,
+  // default -- fastest on one GPU: 33.4 / 29.0 / 24.1 / 17.5 TF/s for 1 / 2 / 4 / 8
+  // at 8192 x 4096 x 8192; 2, 4, 8 cut the peer reads per A element by that factor)
+  static const int cs = [] {
+    const char* e = getenv("BI_KSEG_CLUSTER");
+    const int v = e ? atoi(e) : 1;
+    return (v == 2 || v == 4 || v == 8) ? v : 1;
+  }();
+  TmaSegLaunch L;
+  std::memset(&L, 0, sizeof(L));
+  int64_t k0 = 0;
+  int used = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (kseg[s] == 0) continue;  // empty segments own no k-tile
+    if ((((uintptr_t)a[s]) & 15) || (lda[s] & 1) || k0 % kBK) return false;
+    if (!encode_3d(&L.ta[used], a[s], (uint64_t)kseg[s], (uint64_t)d.M, 1, lda[s], 0, kBK, kBM / cs)) return false;
+    L.kt0[used++] = (int)(k0 / kBK);
+    k0 += kseg[s];
+  }
+  if (!encode_3d(&L.tb, d.B, (uint64_t)d.N, (uint64_t)d.K, 1, d.ldb, 0, 16, kBK)) return false;
+  L.d = d;
+  L.nseg = used;
+  L.tiles_n = (d.N + 63) / 64;
+  L.total_tiles = ((d.M + kBM - 1) / kBM) * L.tiles_n;
+  if (d.M <= 0 || d.N <= 0) return true;
+  const int cap2 = grid_cap > 0 ? 2 * grid_cap : 0;
+  if (cs > 1) {
+    const int groups = ((d.M + kBM - 1) / kBM) * ((L.tiles_n + cs - 1) / cs);
+    const int clusters = (cap2 > 0 && cap2 / cs < groups) ? std::max(1, cap2 / cs) : groups;
+    auto k = cs == 2 ? gemm_tma_kseg_mc_kernel<4, 2> : cs == 8 ? gemm_tma_kseg_mc_kernel<4, 8> : gemm_tma_kseg_mc_kernel<4, 4>;
+    *err = launch_kernel(k, dim3(clusters * cs), dim3(RefillCfg<64>::kThr), (size_t)refill_smem<4, 64>(), stream,
+                         (unsigned)cs, L);
+    return true;
+  }
+  const int grid = (cap2 > 0 && cap2 < L.total_tiles) ? cap2 : L.total_tiles;
+  *err = launch_kernel(gemm_tma_kseg_kernel<4, 64>, dim3(grid), dim3(RefillCfg<64>::kThr),
+                       (size_t)refill_smem<4, 64>(), stream, 1u, L);
+  return true;
+}
 
 // Returns true when the launch was issued with the TMA kernel; false when the
 // descriptors do not qualify (caller falls back to the cp.async kernel).

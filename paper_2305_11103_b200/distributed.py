@@ -54,6 +54,14 @@ class DeviceBackend:
 
         device_gemm(a, b, d, c=c, negate=negate)
 
+    kseg_align = 16  # K1P segment boundaries lie on k-tiles
+
+    def gemm_kseg(self, segs, b, d, c=None, negate=False):
+        """K1P: d = [c] + (+-1) [segs...] @ b, segments read in place (peer GPUs)."""
+        from .core import device_gemm_kseg
+
+        device_gemm_kseg(segs, b, d, c=c, negate=negate)
+
     def inverse(self, blocks, outs):
         """blocks/outs: [count, b, b] strided views; returns the device info
         tensor (no host sync; checked after the run)."""
@@ -145,6 +153,19 @@ class ShardedEngine:
         self.c0 = self.off[self.h0]
         self.w = self.off[self.h1] - self.c0
         self.be = backend if backend is not None else DeviceBackend()
+        # Fused exchange (K1P): with an in-process group whose members can read
+        # each other's memory (local_group.py, peer access over NVLink) and a
+        # backend with gemm_kseg, global-level GEMMs read the peers' column
+        # slabs in place instead of all-gathering them first.
+        import os
+
+        # Opt-in (BI_FUSED_GATHER=1): K1 re-reads each A row block once per
+        # 64-column tile, so at the K1 rate the in-place form needs ~2 TB/s of
+        # peer reads (0.5 TB/s with a 4-CTA multicast cluster) against 0.9 TB/s
+        # per NVLink 5 direction, while the gathered copy costs ~4 % of the
+        # GEMM it feeds (DESIGN 7, profiles/r01_kseg_fused_gather.txt).
+        self.fused = (hasattr(dist, "share") and hasattr(self.be, "gemm_kseg")
+                      and os.environ.get("BI_FUSED_GATHER", "0") == "1")
         # column-slab storage
         self.M = self.be.empty(self.n, self.w)
         self.Minv = self.be.empty(self.n, self.w)
@@ -279,6 +300,33 @@ class ShardedEngine:
         recv = self._allgather_tensor(slab, self.groups[gs], gs)
         return [recv[i][:, :self._width(m)] for i, m in enumerate(members)], members
 
+    def _fusable(self, lv, act, in_a) -> bool:
+        """K1P applies when the owners' slab widths put every segment boundary
+        on a k-tile, the group has at most 8 owners per half, and no shared
+        slab is overwritten by this level's outputs (sources other than T_lv)."""
+        if not self.fused:
+            return False
+        if act is not None and act.source != "matrix" and act.cid == lv:
+            return False
+        gs = (1 << lv) // self.nbp
+        members = _group_ranks(self.rank, gs)
+        if gs // 2 > 8:
+            return False
+        align = getattr(self.be, "kseg_align", 1)
+        half = [m for m in members if (self._rank_h1(m) <= self._quad(lv, self.h0 >> lv)[1]) == in_a]
+        other = [m for m in members if m not in half]
+        return all(self._width(m) % align == 0 for grp in (half, other) for m in grp[:-1])
+
+    def _share(self, level, value):
+        """Publish this rank's slab views inside its level group; returns every
+        member's views (producer streams done) and the member ranks."""
+        gs = (1 << level) // self.nbp
+        return self.dist.share(value, group=self.groups[gs]), _group_ranks(self.rank, gs)
+
+    def _release(self, level):
+        """Every member done reading before any owner overwrites a shared slab."""
+        self.dist.release(group=self.groups[(1 << level) // self.nbp])
+
     def _arrows(self, act):
         lv = act.sid
         be = self.be
@@ -315,6 +363,21 @@ class ShardedEngine:
         else:
             top = self.src_win(act, first, mid, *mine)
             bot = self.minv_win(mid, last, *mine)
+        if self._fusable(lv, act, in_a):
+            # peers' A^-1 / B / C / D^-1 column slabs are K segments of K1P, read in place
+            shared, members = self._share(lv, (top, bot))
+            peers = [i for i, m in enumerate(members) if (self._rank_h1(m) <= mid) != in_a]
+            tops, bots = [shared[i][0] for i in peers], [shared[i][1] for i in peers]
+            if in_a:  # L = -D^-1 C, S_D = A + B L (my columns)
+                L_my = self.t_win(lv, mid, last, *mine)
+                self.be.gemm_kseg(bots, self.src_win(act, mid, last, *mine), L_my, negate=True)
+                self.be.gemm_kseg(tops, L_my, self.t_win(lv, first, mid, *mine), c=self.src_win(act, first, mid, *mine))
+            else:     # R = -A^-1 B, S_A = D + C R (my columns)
+                R_my = self.t_win(lv, first, mid, *mine)
+                self.be.gemm_kseg(tops, self.src_win(act, first, mid, *mine), R_my, negate=True)
+                self.be.gemm_kseg(bots, R_my, self.t_win(lv, mid, last, *mine), c=self.src_win(act, mid, last, *mine))
+            self._release(lv)
+            return
         slab = torch.cat([top, bot], dim=0)
         recv, members = self._allgather(lv, slab)
         peers = [i for i, m in enumerate(members) if (self._rank_h1(m) <= mid) != in_a]
@@ -361,6 +424,15 @@ class ShardedEngine:
         hmax = max(ha, hd)
         # A-half ranks carry their L columns (C position), D-half ranks their R columns
         part = self.t_win(lv, mid, last, *mine) if in_a else self.t_win(lv, first, mid, *mine)
+        if self._fusable(lv, None, in_a):
+            shared, members = self._share(lv, part)
+            segs = [shared[i] for i, m in enumerate(members) if (self._rank_h1(m) <= mid) == in_a]
+            if in_a:  # M_inv[D, A] = L M_inv[A, A]
+                be.gemm_kseg(segs, self.minv_win(first, mid, *mine), self.minv_win(mid, last, *mine))
+            else:     # M_inv[A, D] = R M_inv[D, D]
+                be.gemm_kseg(segs, self.minv_win(mid, last, *mine), self.minv_win(first, mid, *mine))
+            self._release(lv)
+            return
         slab = torch.zeros((hmax, part.shape[1]), dtype=part.dtype, device=part.device)
         slab[:part.shape[0]] = part
         recv, members = self._allgather(lv, slab)

@@ -97,6 +97,27 @@ class LocalDist:
             torch.cuda.current_stream(recv.device).synchronize()
         group.barrier.wait()  # every receiver done before any sender reuses its buffer
 
+    def share(self, value, group=None) -> list:
+        """Fused-exchange hand-off (K1P): publish ``value`` (device views) and
+        return every member's, in member order, once every producer stream is
+        done.  Readers access the peers' memory directly (peer access over
+        NVLink); must be paired with ``release``."""
+        import torch
+
+        group = group or self.world.world
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()  # producer done
+        _, slots = self._exchange(group, value)
+        return slots
+
+    def release(self, group=None) -> None:
+        """Every reader's kernels done before any owner reuses its buffers."""
+        import torch
+
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+        (group or self.world.world).barrier.wait()
+
     def all_gather(self, parts, tensor, group=None) -> None:
         group = group or self.world.world
         _, slots = self._exchange(group, tensor)

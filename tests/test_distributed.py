@@ -126,6 +126,41 @@ def test_local_threads_schedule_cpu(gpus, sizes):
     assert np.max(np.abs(out - ref)) <= 1e-12 * n
 
 
+class FusedCPUBackend(TorchCPUBackend):
+    """TorchCPUBackend plus the K1P entry (segments concatenated on the host):
+    drives the fused-exchange schedule (share -> in-place segment reads ->
+    release) on CPU threads."""
+
+    kseg_align = 1
+    calls = 0
+
+    def gemm_kseg(self, segs, b, d, c=None, negate=False):
+        type(self).calls += 1
+        self.gemm(torch.cat(list(segs), dim=1), b, d, c=c, negate=negate)
+
+
+@pytest.mark.parametrize("gpus,sizes,align", [(2, [6] * 4, 1), (4, [8] * 8, 1), (4, [2, 7, 5, 3, 6, 4, 9, 1], 1),
+                                              (4, [4, 4, 5, 3, 6, 2, 4, 4], 8)])
+def test_local_threads_fused_exchange_cpu(monkeypatch, gpus, sizes, align):
+    """Global levels read the peers' slabs as K segments (no gathered copy);
+    same inverse as the oracle engine.  With align=8 the ragged group whose
+    first owner is 8 wide fuses and the rest falls back to the all-gather."""
+    from paper_2305_11103_b200.distributed import run_inversion_local
+
+    monkeypatch.setenv("BI_FUSED_GATHER", "1")
+
+    class B(FusedCPUBackend):
+        kseg_align = align
+        calls = 0
+
+    n = sum(sizes)
+    m = well_conditioned(n, 970 + n)
+    out = run_inversion_local(m, sizes, gpus, backend_factory=B, devices=[None] * gpus)
+    ref = oracle.run_inversion(m, sizes=sizes, leaf_inverter=oracle.gauss_jordan)
+    assert np.max(np.abs(out - ref)) <= 1e-12 * n
+    assert B.calls > 0
+
+
 def test_local_threads_failure_does_not_hang():
     from paper_2305_11103_b200.distributed import run_inversion_local
 
@@ -165,3 +200,32 @@ def test_local_threads_two_on_one_gpu_bitwise():
     out = run_inversion_local(m, sizes, 2, devices=[0, 0])
     single = bi.run_inversion(m, sizes=sizes).to_dense()
     assert np.array_equal(out, single)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gpus,sizes,fused", [(2, [64] * 8, "1"), (2, [64] * 8, "0"), (4, [128] * 8, "1"),
+                                              (4, [40, 24, 64, 56, 72, 8, 48, 32], "1")])
+def test_local_threads_fused_gather_bitwise(monkeypatch, gpus, sizes, fused):
+    """K1P inside the thread-per-GPU schedule (threads sharing the B200, each
+    reading the others' slabs through their device pointers): bitwise equal
+    to the single-device engine, fused (BI_FUSED_GATHER=1, opt-in) or with
+    the gathered copies (0, default); the fused run really takes K1P."""
+    import paper_2305_11103_b200 as bi
+    from paper_2305_11103_b200 import distributed
+    from paper_2305_11103_b200.distributed import run_inversion_local
+
+    monkeypatch.setenv("BI_FUSED_GATHER", fused)
+    calls = []
+    orig = distributed.DeviceBackend.gemm_kseg
+
+    def counting(self, *a, **k):
+        calls.append(1)
+        return orig(self, *a, **k)
+
+    monkeypatch.setattr(distributed.DeviceBackend, "gemm_kseg", counting)
+    n = sum(sizes)
+    m = well_conditioned(n, 79 + gpus)
+    out = run_inversion_local(m, sizes, gpus, devices=[0] * gpus)
+    single = bi.run_inversion(m, sizes=sizes).to_dense()
+    assert np.array_equal(out, single)
+    assert (len(calls) > 0) == (fused == "1")

@@ -45,6 +45,88 @@ def test_gemm_vs_numpy(bi, m, n, k, negate, accumulate):
     assert np.linalg.norm(got - ref) <= _gemm_tol(a, b, c if accumulate else None, k)
 
 
+@pytest.mark.parametrize("m,n,widths", [(128, 64, [16]), (300, 257, [64, 128, 32, 7]), (129, 70, [16, 16, 16, 16, 16, 16, 16, 1]),
+                                         (512, 512, [256, 256]), (77, 33, [48, 0, 32]), (5, 3, [0])])
+@pytest.mark.parametrize("negate,accumulate", [(False, False), (True, True)])
+def test_gemm_kseg_bitwise(bi, m, n, widths, negate, accumulate):
+    """K1P (segments read in place, as from peer GPUs) is bitwise equal to K1
+    on the gathered operand, and within the GEMM tolerance of NumPy."""
+    import torch
+
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.core import device_gemm, device_gemm_kseg
+
+    g = np.random.default_rng(m + n + sum(widths))
+    k = sum(widths)
+    segs_h = [g.standard_normal((m, w)) for w in widths]
+    b, c = g.standard_normal((k, n)), g.standard_normal((m, n))
+    segs = [_lib.to_device(x) for x in segs_h]
+    db = _lib.to_device(b)
+    d1, d2 = _lib.to_device(c), _lib.to_device(c)
+    device_gemm_kseg(segs, db, d1, c=d1 if accumulate else None, negate=negate)
+    a = np.concatenate(segs_h, axis=1) if k else np.zeros((m, 0))
+    device_gemm(_lib.to_device(a) if k else _lib.empty_matrix(m, 0), db, d2, c=d2 if accumulate else None, negate=negate)
+    torch.cuda.synchronize()
+    got = d1.cpu().numpy()
+    assert np.array_equal(got, d2.cpu().numpy())
+    ref = (c if accumulate else 0.0) + (-1.0 if negate else 1.0) * (a @ b)
+    assert np.linalg.norm(got - ref) <= _gemm_tol(a, b, c if accumulate else None, k)
+
+
+_KSEG_SCRIPT = """
+import numpy as np, torch
+from paper_2305_11103_b200 import _lib
+from paper_2305_11103_b200.core import device_gemm, device_gemm_kseg
+g = np.random.default_rng(3)
+for m, n, widths in [(1000, 700, [256, 256, 64, 200]), (128, 64, [16]), (300, 1000, [512, 512, 512, 512, 512, 512, 512, 77])]:
+    segs_h = [g.standard_normal((m, w)) for w in widths]
+    b = g.standard_normal((sum(widths), n)); c = g.standard_normal((m, n))
+    d1, d2 = _lib.to_device(c), _lib.to_device(c)
+    db = _lib.to_device(b)
+    device_gemm_kseg([_lib.to_device(x) for x in segs_h], db, d1, c=d1, negate=True)
+    device_gemm(_lib.to_device(np.concatenate(segs_h, axis=1)), db, d2, c=d2, negate=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(d1.cpu().numpy(), d2.cpu().numpy()), (m, n, widths)
+print("KSEG OK")
+"""
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "4", "8"])
+def test_gemm_kseg_cluster_multicast_bitwise(bi, cluster):
+    """Every K1P cluster size (TMA multicast of the A slices across 2/4/8 CTAs;
+    1 = no cluster) is bitwise equal to K1 on the gathered operand, including
+    cluster padding tiles past N and ragged M/K tails."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, BI_KSEG_CLUSTER=cluster)
+    r = subprocess.run([sys.executable, "-c", _KSEG_SCRIPT], env=env, capture_output=True, text=True, timeout=240,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "KSEG OK" in r.stdout, r.stderr[-2000:]
+
+
+def test_gemm_kseg_unaligned_and_errors(bi):
+    """Odd-offset segment views take the 8-byte path; a segment boundary off a
+    k-tile is rejected (DimensionMismatch), not silently re-tiled."""
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.core import device_gemm, device_gemm_kseg
+    from paper_2305_11103_b200.errors import DimensionMismatch
+
+    g = np.random.default_rng(9)
+    big = _lib.to_device(g.standard_normal((301, 303)))
+    segs = [big[1:200, 3:35], big[1:200, 101:150]]
+    b = big[5:86, 7:160]
+    out, ref = _lib.empty_matrix(199, 153), _lib.empty_matrix(199, 153)
+    device_gemm_kseg(segs, b, out)
+    import torch
+
+    device_gemm(torch.cat(segs, dim=1).contiguous(), b, ref)
+    assert np.array_equal(out.cpu().numpy(), ref.cpu().numpy())
+    with pytest.raises(DimensionMismatch):
+        device_gemm_kseg([big[:10, :20], big[:10, 20:40]], big[:40, :8], _lib.empty_matrix(10, 8))
+
+
 def test_gemm_unaligned_views(bi):
     """Odd leading dimensions / odd column offsets take the 8-byte copy path."""
     from paper_2305_11103_b200 import _lib
