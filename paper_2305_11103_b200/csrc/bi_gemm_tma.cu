@@ -342,9 +342,11 @@ __global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks
 // instead of once per column tile (remote reads are not cached in the reading
 // GPU's L2; at the K1 rate one column tile per A fetch needs ~2 TB/s, with
 // CS = 4 about 0.5 TB/s, under one NVLink 5 direction).  A stage is refilled
-// only when every CTA of the cluster released it: each CTA's last releasing
-// warp arrives on the `empty` barrier of every cluster CTA, then waits on its
-// own.  Same stage layout, k order and epilogue as K1: bitwise equal.
+// only when every CTA of the cluster released it (cluster-wide `empty`
+// barriers, below).  Same stage layout, k order and epilogue as K1: bitwise
+// equal.  Measured on one B200 (local segments): 28.6 / 25.5 / 17.9 TF/s at
+// CS = 2 / 4 / 8 against 33.4 without a cluster, with blocking and with
+// non-blocking refills alike (profiles/r01_kseg_fused_gather.txt).
 __device__ __forceinline__ unsigned cluster_ctarank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -358,17 +360,6 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, unsigned cta) 
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
 }
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                                unsigned short mask) {
   asm volatile(
@@ -378,6 +369,26 @@ __device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map
       : "memory");
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+// No warp ever blocks on the cluster: the last releasing warp of a stage only
+// arrives (remotely) on every cluster CTA's `empty` barrier; refills are
+// issued in order by whichever warp's lane 0 first sees the next one's
+// `empty` phase complete (a shared cursor, claimed by CAS) -- before each
+// k-step and while spinning on a `full` barrier.  Iteration u of a CTA is
+// stage u % kStages of tile cid + (u / KT) * ncl, k-tile u % KT.
 template <int kStages, int CS>
 __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks)
     gemm_tma_kseg_mc_kernel(const __grid_constant__ TmaSegLaunch L) {
@@ -389,6 +400,7 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ unsigned released[kStages];
+  __shared__ unsigned next_fill;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp / (TN / 32), wn = warp % (TN / 32);
@@ -400,6 +412,7 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
       mbar_init(&empty[s], CS);
       released[s] = 0;
     }
+    next_fill = kStages;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -412,12 +425,11 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
   const int groups_n = (L.tiles_n + CS - 1) / CS;
   const int total_ct = ((d.M + kBM - 1) / kBM) * groups_n;
   const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+  const unsigned iters = cid < total_ct ? (unsigned)((total_ct - cid + ncl - 1) / ncl) * (unsigned)KT : 0u;
   const unsigned short mask = (unsigned short)((1u << CS) - 1);
 
-  auto fill = [&](int stage, int ct, int ahead) {
-    ct += (ahead / KT) * ncl;
-    ahead %= KT;
-    if (ct >= total_ct) return;
+  auto fill = [&](unsigned u) {
+    const int stage = u % kStages, ct = cid + (int)(u / KT) * ncl, ahead = u % KT;
     int s = 0;
     while (s + 1 < L.nseg && L.kt0[s + 1] <= ahead) ++s;
     const int m0 = (ct / groups_n) * kBM, n0 = ((ct % groups_n) * CS + (int)crank) * TN;
@@ -430,8 +442,14 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
 #pragma unroll
     for (int j = 0; j < TN / 16; ++j) tma_load_3d(sb + j * kBoxBBytes, &L.tb, &full[stage], n0 + 16 * j, ahead * kBK, 0);
   };
-  if (tid == 0 && cid < total_ct)
-    for (int s = 0; s < kStages; ++s) fill(s, cid, s);
+  // issue the next refill if the whole cluster released its stage (lane 0s only)
+  auto poll = [&]() {
+    const unsigned u = *reinterpret_cast<volatile unsigned*>(&next_fill);
+    if (u < iters && mbar_test(&empty[u % kStages], ((u / kStages) - 1) & 1) && atomicCAS(&next_fill, u, u + 1) == u)
+      fill(u);
+  };
+  if (tid == 0)
+    for (unsigned u = 0; u < (unsigned)kStages && u < iters; ++u) fill(u);
 
   unsigned cons_it = 0;
   for (int ct = cid; ct < total_ct; ct += ncl) {
@@ -442,15 +460,18 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int kt = 0; kt < KT; ++kt) {
       const int stage = cons_it % kStages;
-      mbar_wait(&full[stage], (cons_it / kStages) & 1);
+      const unsigned par = (cons_it / kStages) & 1;
+      if (lane == 0) poll();
+      while (!mbar_test(&full[stage], par)) {
+        if (lane == 0) poll();
+      }
       k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
       __syncwarp();
       if (lane == 0 && atomicAdd(&released[stage], 1u) == Cfg::kWarpsT - 1) {
         released[stage] = 0;
-        if (ct + ((kt + kStages) / KT) * ncl < total_ct) {  // a refill follows (same test in every CTA)
+        if (cons_it + kStages < iters) {  // a refill follows (same test in every CTA)
           for (int r = 0; r < CS; ++r) mbar_arrive_remote(&empty[stage], r);
-          mbar_wait_cluster(&empty[stage], (cons_it / kStages) & 1);
-          fill(stage, ct, kt + kStages);
+          poll();
         }
       }
       ++cons_it;
