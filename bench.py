@@ -133,21 +133,55 @@ def _ref_sample_worker(seed: int) -> float:
     return time.perf_counter() - t0
 
 
-def reference_sample_step(procs: int) -> tuple[float, float]:
-    """Invert a batch of BATCH sample matrices with the reference algorithm,
-    `procs` processes in parallel (the reference engine itself is
-    single-threaded: its per-k ufunc loop is GIL-bound).
-    Returns (wall seconds, nominal flops)."""
+def _ref_warm(_: int) -> None:
+    import oracle
+
+    g = np.random.default_rng(0)
+    oracle.run_inversion(g.standard_normal((64, 64)) + 64 * np.eye(64), sizes=[8] * 8)
+
+
+def host_threads() -> int:
+    """Host threads this process may run on (affinity-aware)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def sample_count(procs: int) -> int:
+    """Sample matrices per step: the batch, widened to keep every process busy."""
+    return max(BATCH, procs)
+
+
+def reference_pool(procs: int):
+    """Worker processes for the reference arm, started outside the timed
+    region (None for a single process)."""
     import multiprocessing as mp
 
-    t0 = time.perf_counter()
-    if procs <= 1:
-        for b in range(BATCH):
-            _ref_sample_worker(b)
-    else:
-        with mp.get_context("fork").Pool(procs) as pool:
-            pool.map(_ref_sample_worker, range(BATCH))
-    return time.perf_counter() - t0, BATCH * nominal_flops(SAMPLE_N)
+    return mp.get_context("fork").Pool(procs) if procs > 1 else None
+
+
+def reference_sample_step(procs: int, pool=None) -> tuple[float, float]:
+    """Invert sample_count(procs) sample matrices with the reference
+    algorithm, `procs` processes in parallel, one matrix per process at a
+    time (the reference engine itself is single-threaded: its per-k ufunc
+    loop is GIL-bound), so the arm uses every host thread.
+    Returns (wall seconds, nominal flops)."""
+    count = sample_count(procs)
+    own = pool is None and procs > 1
+    if own:
+        pool = reference_pool(procs)
+    try:
+        t0 = time.perf_counter()
+        if pool is None:
+            for b in range(count):
+                _ref_sample_worker(b)
+        else:
+            pool.map(_ref_sample_worker, range(count), chunksize=1)
+        return time.perf_counter() - t0, count * nominal_flops(SAMPLE_N)
+    finally:
+        if own:
+            pool.close()
 
 
 def run_reference_arm(args) -> None:
@@ -155,7 +189,7 @@ def run_reference_arm(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    procs = max(1, min(BATCH, os.cpu_count() or 1))
+    procs = host_threads()
     for _ in range(args.warmup):  # untimed warm-up: tiny problem (imports, page-in)
         import oracle
 
@@ -164,20 +198,27 @@ def run_reference_arm(args) -> None:
         oracle.run_inversion(m, sizes=[8] * 8)
     times = []
     flops = 0.0
-    for _ in range(args.steps):
-        dt, flops = reference_sample_step(procs)
-        times.append(dt)
+    pool = reference_pool(procs)
+    try:
+        if pool is not None:
+            pool.map(_ref_warm, range(procs), chunksize=1)  # workers forked and numpy paged in
+        for _ in range(args.steps):
+            dt, flops = reference_sample_step(procs, pool)
+            times.append(dt)
+    finally:
+        if pool is not None:
+            pool.close()
     total = sum(times)
     value = flops * args.steps / total / 1e12
-    sample = (f"{BATCH} matrices of n={SAMPLE_N} (8 blocks of {SAMPLE_SIZES[0]}, same generator family) per step, "
+    sample = (f"{sample_count(procs)} matrices of n={SAMPLE_N} (8 blocks of {SAMPLE_SIZES[0]}, same generator family) per step, "
               f"reference run_inversion algorithm (oracle/ port, op-for-op), {procs} processes")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample_n": SAMPLE_N, "batch": BATCH},
-        "s_per_inverse": total / (args.steps * BATCH),
-        "s_per_inverse_n4096_extrapolated_n3": total / (args.steps * BATCH) * (N / SAMPLE_N) ** 3,
+        "s_per_inverse": total / (args.steps * sample_count(procs)),
+        "s_per_inverse_n4096_extrapolated_n3": total / (args.steps * sample_count(procs)) * (N / SAMPLE_N) ** 3,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -337,14 +378,21 @@ def run_gpu_arm(args) -> None:
     # ---- CPU baseline (rank 0, N=1): reference algorithm on a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        procs = max(1, min(BATCH, os.cpu_count() or 1))
+        procs = host_threads()
         # bounded sample, repeated to >= 10 s of CPU work (at most 8 rounds)
         dt, fl, rounds = 0.0, 0.0, 0
-        while rounds < 8 and (rounds == 0 or dt < 10.0):
-            d1, f1 = reference_sample_step(procs)
-            dt, fl, rounds = dt + d1, fl + f1, rounds + 1
+        pool = reference_pool(procs)
+        try:
+            if pool is not None:
+                pool.map(_ref_warm, range(procs), chunksize=1)
+            while rounds < 8 and (rounds == 0 or dt < 10.0):
+                d1, f1 = reference_sample_step(procs, pool)
+                dt, fl, rounds = dt + d1, fl + f1, rounds + 1
+        finally:
+            if pool is not None:
+                pool.close()
         cpu = {"value": fl / dt / 1e12, "unit": UNIT, "cores": procs, "kind": "port",
-               "sample": f"{rounds} x {BATCH} matrices n={SAMPLE_N} (8 blocks of {SAMPLE_SIZES[0]}) through the "
+               "sample": f"{rounds} x {sample_count(procs)} matrices n={SAMPLE_N} (8 blocks of {SAMPLE_SIZES[0]}) through the "
                          f"reference run_inversion algorithm (oracle/ port, op-for-op), {procs} processes, "
                          f"{dt:.1f} s"}
 
