@@ -336,17 +336,17 @@ __global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks
 }
 
 // K1P with TMA multicast across a thread-block cluster of CS CTAs that share
-// one A row block (consecutive 64-column tiles): each CTA loads 128/CS rows of
-// the A k-tile and multicasts them into every CTA of the cluster, so each A
+// one A row block (consecutive 64-column tiles): the cluster's leader loads
+// the A k-tile once and multicasts it into every CTA of the cluster, so each A
 // element -- a peer's slab, read over NVLink -- is fetched once per cluster
 // instead of once per column tile (remote reads are not cached in the reading
 // GPU's L2; at the K1 rate one column tile per A fetch needs ~2 TB/s, with
 // CS = 4 about 0.5 TB/s, under one NVLink 5 direction).  A stage is refilled
 // only when every CTA of the cluster released it (cluster-wide `empty`
 // barriers, below).  Same stage layout, k order and epilogue as K1: bitwise
-// equal.  Measured on one B200 (local segments): 28.6 / 25.5 / 17.9 TF/s at
-// CS = 2 / 4 / 8 against 33.4 without a cluster, with blocking and with
-// non-blocking refills alike (profiles/r01_kseg_fused_gather.txt).
+// equal.  Measured on one B200 (local segments): 30.5 / 29.4 / 26.7 TF/s at
+// CS = 2 / 4 / 8 against 33.4 without a cluster (per-CTA slices + all-to-all
+// empty arrives had given 28.6 / 25.5 / 17.9; profiles/r01_kseg_fused_gather.txt).
 __device__ __forceinline__ unsigned cluster_ctarank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -383,18 +383,18 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned phase) {
   return ok != 0;
 }
 
-// No warp ever blocks on the cluster: the last releasing warp of a stage only
-// arrives (remotely) on every cluster CTA's `empty` barrier; refills are
-// issued in order by whichever warp's lane 0 first sees the next one's
-// `empty` phase complete (a shared cursor, claimed by CAS) -- before each
-// k-step and while spinning on a `full` barrier.  Iteration u of a CTA is
-// stage u % kStages of tile cid + (u / KT) * ncl, k-tile u % KT.
+// Leader-issued A: CTA rank 0 multicasts the whole 128-row A k-tile to the
+// cluster once every CTA released the stage (one remote arrive per CTA on the
+// leader's `empty` barrier; the leader's warps poll it, in order, before each
+// k-step and while spinning on a `full` barrier -- no warp blocks on the
+// cluster).  Each CTA refills its own B boxes the moment its own warps
+// released the stage.  Iteration u of a CTA is stage u % kStages of tile
+// cid + (u / KT) * ncl, k-tile u % KT.
 template <int kStages, int CS>
 __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks)
     gemm_tma_kseg_mc_kernel(const __grid_constant__ TmaSegLaunch L) {
   pdl_enter();
   constexpr int TN = 64;
-  constexpr int kSlice = kBM / CS;  // A rows each CTA loads and multicasts
   using Cfg = RefillCfg<TN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
   const int wm = warp / (TN / 32), wn = warp % (TN / 32);
   const int fr = lane >> 2, fc = lane & 3;
   const unsigned crank = cluster_ctarank();
+  const bool leader = crank == 0;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -428,28 +429,32 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
   const unsigned iters = cid < total_ct ? (unsigned)((total_ct - cid + ncl - 1) / ncl) * (unsigned)KT : 0u;
   const unsigned short mask = (unsigned short)((1u << CS) - 1);
 
-  auto fill = [&](unsigned u) {
+  auto fill_b = [&](unsigned u) {  // this CTA's B boxes (+ the stage's expected bytes)
     const int stage = u % kStages, ct = cid + (int)(u / KT) * ncl, ahead = u % KT;
-    int s = 0;
-    while (s + 1 < L.nseg && L.kt0[s + 1] <= ahead) ++s;
-    const int m0 = (ct / groups_n) * kBM, n0 = ((ct % groups_n) * CS + (int)crank) * TN;
+    const int n0 = ((ct % groups_n) * CS + (int)crank) * TN;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    uint8_t* sa = smem + stage * Cfg::kStage;
-    uint8_t* sb = sa + kStageA;
-    mbar_expect_tx(&full[stage], Cfg::kStage);  // all CS A slices + this CTA's B boxes
-    tma_load_3d_mc(sa + crank * kSlice * 128, &L.ta[s], &full[stage], (ahead - L.kt0[s]) * kBK, m0 + crank * kSlice, 0,
-                   mask);
+    uint8_t* sb = smem + stage * Cfg::kStage + kStageA;
+    mbar_expect_tx(&full[stage], Cfg::kStage);  // the multicast A k-tile + this CTA's B boxes
 #pragma unroll
     for (int j = 0; j < TN / 16; ++j) tma_load_3d(sb + j * kBoxBBytes, &L.tb, &full[stage], n0 + 16 * j, ahead * kBK, 0);
   };
-  // issue the next refill if the whole cluster released its stage (lane 0s only)
-  auto poll = [&]() {
+  auto fill_a = [&](unsigned u) {  // leader: the A k-tile into every CTA of the cluster
+    const int stage = u % kStages, ct = cid + (int)(u / KT) * ncl, ahead = u % KT;
+    int s = 0;
+    while (s + 1 < L.nseg && L.kt0[s + 1] <= ahead) ++s;
+    tma_load_3d_mc(smem + stage * Cfg::kStage, &L.ta[s], &full[stage], (ahead - L.kt0[s]) * kBK,
+                   (ct / groups_n) * kBM, 0, mask);
+  };
+  auto poll = [&]() {  // leader lane 0s: next A refill once the whole cluster released its stage
     const unsigned u = *reinterpret_cast<volatile unsigned*>(&next_fill);
     if (u < iters && mbar_test(&empty[u % kStages], ((u / kStages) - 1) & 1) && atomicCAS(&next_fill, u, u + 1) == u)
-      fill(u);
+      fill_a(u);
   };
   if (tid == 0)
-    for (unsigned u = 0; u < (unsigned)kStages && u < iters; ++u) fill(u);
+    for (unsigned u = 0; u < (unsigned)kStages && u < iters; ++u) {
+      fill_b(u);
+      if (leader) fill_a(u);
+    }
 
   unsigned cons_it = 0;
   for (int ct = cid; ct < total_ct; ct += ncl) {
@@ -461,17 +466,18 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
     for (int kt = 0; kt < KT; ++kt) {
       const int stage = cons_it % kStages;
       const unsigned par = (cons_it / kStages) & 1;
-      if (lane == 0) poll();
+      if (leader && lane == 0) poll();
       while (!mbar_test(&full[stage], par)) {
-        if (lane == 0) poll();
+        if (leader && lane == 0) poll();
       }
       k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
       __syncwarp();
       if (lane == 0 && atomicAdd(&released[stage], 1u) == Cfg::kWarpsT - 1) {
         released[stage] = 0;
         if (cons_it + kStages < iters) {  // a refill follows (same test in every CTA)
-          for (int r = 0; r < CS; ++r) mbar_arrive_remote(&empty[stage], r);
-          poll();
+          mbar_arrive_remote(&empty[stage], 0);
+          fill_b(cons_it + kStages);
+          if (leader) poll();
         }
       }
       ++cons_it;
@@ -550,7 +556,7 @@ bool launch_gemm_kseg_tma(const GemmDesc& d, int nseg, const double* const* a, c
   if (nseg < 1 || nseg > kMaxKSeg || d.K <= 0 || tma_init() != cudaSuccess) return false;
   if ((((uintptr_t)d.B) & 15) || (d.ldb & 1)) return false;
   // BI_KSEG_CLUSTER: CTAs per cluster sharing A by TMA multicast (1: no cluster,
-  // default -- fastest on one GPU: 33.4 / 29.0 / 24.1 / 17.5 TF/s for 1 / 2 / 4 / 8
+  // default -- fastest on one GPU: 33.4 / 30.5 / 29.4 / 26.7 TF/s for 1 / 2 / 4 / 8
   // at 8192 x 4096 x 8192; 2, 4, 8 cut the peer reads per A element by that factor)
   static const int cs = [] {
     const char* e = getenv("BI_KSEG_CLUSTER");
@@ -564,7 +570,7 @@ bool launch_gemm_kseg_tma(const GemmDesc& d, int nseg, const double* const* a, c
   for (int s = 0; s < nseg; ++s) {
     if (kseg[s] == 0) continue;  // empty segments own no k-tile
     if ((((uintptr_t)a[s]) & 15) || (lda[s] & 1) || k0 % kBK) return false;
-    if (!encode_3d(&L.ta[used], a[s], (uint64_t)kseg[s], (uint64_t)d.M, 1, lda[s], 0, kBK, kBM / cs)) return false;
+    if (!encode_3d(&L.ta[used], a[s], (uint64_t)kseg[s], (uint64_t)d.M, 1, lda[s], 0, kBK, kBM)) return false;
     L.kt0[used++] = (int)(k0 / kBK);
     k0 += kseg[s];
   }
