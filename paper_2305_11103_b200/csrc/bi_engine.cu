@@ -20,12 +20,14 @@
 //  * singular leaves are recorded per diag step on the device and resolved
 //    to (step, quad, matrix) after the range (no host syncs inside it).
 #include <algorithm>
+#include <array>
 #include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -229,8 +231,18 @@ struct bi_engine {
 
   void* meta_dev = nullptr;
   int64_t meta_cap = 0;
+  // page-locked staging for pageable host buffers (bi_engine_run_host):
+  // [Z][n][ldm] input, [Z][n][ldi] output, allocated on first use
+  double* stage_in = nullptr;
+  double* stage_out = nullptr;
+  int64_t stage_in_bytes = 0, stage_out_bytes = 0;
+  cudaEvent_t ev_level[32] = {};  // H2D of input level l done (pipelined host path)
 
   ~bi_engine() {
+    if (stage_in) cudaFreeHost(stage_in);
+    if (stage_out) cudaFreeHost(stage_out);
+    for (cudaEvent_t ev : ev_level)
+      if (ev) cudaEventDestroy(ev);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (capture_stream) cudaStreamDestroy(capture_stream);
     for (int l = 0; l < kMaxLanes; ++l) {
@@ -1109,6 +1121,195 @@ extern "C" int bi_engine_run(bi_engine* e, int first_step, int last_step, int us
   return run_impl(e, first_step, last_step, use_graph, static_cast<cudaStream_t>(stream), nullptr);
 }
 
+// ---------------------------------------------------------------------------
+// Pageable host buffers (a plain NumPy array through the drop-in call).
+// A pageable cudaMemcpy runs at ~11 GB/s and cannot be captured; copying the
+// whole input into page-locked memory first serialises a host copy, the DMA
+// and the compute.  Instead the input moves in NEED ORDER, level by level
+// (step 1 reads only the diagonal blocks, step 2^l first reads the level-l
+// quads' B and C blocks): the host copies level l into engine-owned
+// page-locked staging (all host threads), DMAs it on the copy stream, and
+// the steps [2^l, 2^(l+1)) -- each range one cached CUDA graph -- wait only
+// for that level.  While the device runs range l the host stages level l+1.
+// A page-locked output is read back inside the last range's graph (top
+// quads during the last pass); a pageable output goes through page-locked
+// staging and is copied out after the stream drains.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Region {
+  char* dst;
+  const char* src;
+  int64_t dld, sld;  // bytes
+  int64_t rows, bytes;
+};
+
+// dst/src 2-D regions copied by up to `threads` host threads, split by rows
+static void par_copy(const std::vector<Region>& regs, int threads) {
+  int64_t total = 0;
+  for (const Region& r : regs) total += r.rows * r.bytes;
+  if (total == 0) return;
+  const int64_t per = 4 << 20;
+  int T = (int)std::max<int64_t>(1, std::min<int64_t>(threads, total / per));
+  if (T == 1) {
+    for (const Region& r : regs)
+      for (int64_t i = 0; i < r.rows; ++i) std::memcpy(r.dst + i * r.dld, r.src + i * r.sld, r.bytes);
+    return;
+  }
+  // contiguous byte ranges of the concatenated rows, one per thread
+  auto work = [&](int t) {
+    const int64_t b0 = total * t / T, b1 = total * (t + 1) / T;
+    int64_t pos = 0;
+    for (const Region& r : regs) {
+      const int64_t sz = r.rows * r.bytes;
+      if (pos + sz <= b0) {
+        pos += sz;
+        continue;
+      }
+      if (pos >= b1) break;
+      for (int64_t i = 0; i < r.rows; ++i) {
+        const int64_t r0 = pos + i * r.bytes, r1 = r0 + r.bytes;
+        const int64_t lo = std::max(r0, b0), hi = std::min(r1, b1);
+        if (lo < hi) std::memcpy(r.dst + i * r.dld + (lo - r0), r.src + i * r.sld + (lo - r0), hi - lo);
+      }
+      pos += sz;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+}
+
+static int host_threads() {
+  static const int n = [] {
+    const char* v = getenv("BI_HOST_THREADS");
+    int t = v ? atoi(v) : (int)std::thread::hardware_concurrency();
+    return std::max(1, std::min(t, 32));
+  }();
+  return n;
+}
+
+}  // namespace
+
+// input blocks first read at level lv: the diagonal blocks (lv = 0) or the
+// level-lv quads' off-diagonal B and C blocks
+static void level_blocks(const bi_engine* e, int lv, std::vector<std::array<int, 4>>& out) {
+  out.clear();
+  if (lv == 0) {
+    for (int p = 0; p < e->nb; ++p) out.push_back({p, p + 1, p, p + 1});
+    return;
+  }
+  for (int g = 0; g < (e->nb >> lv); ++g) {
+    const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+    out.push_back({first, mid, mid, last});
+    out.push_back({mid, last, first, mid});
+  }
+}
+
+static int run_host_pipelined(bi_engine* e, const double* in, int64_t ld_in, int64_t s_in, double* out,
+                              int64_t ld_out, int64_t s_out, int last_step, int use_graph, cudaStream_t s) {
+  const bool in_pinned = is_pinned(in), out_pinned = is_pinned(out);
+  const int64_t n = e->n;
+  const int T = host_threads();
+  const int64_t in_bytes = (int64_t)e->Z * n * e->ldm * 8, out_bytes = (int64_t)e->Z * n * e->ldi * 8;
+  if (in && !in_pinned && e->stage_in_bytes < in_bytes) {
+    if (e->stage_in) cudaFreeHost(e->stage_in);
+    e->stage_in = nullptr;
+    e->stage_in_bytes = 0;
+    BI_CUDA_TRY(cudaHostAlloc((void**)&e->stage_in, in_bytes, cudaHostAllocPortable));
+    e->stage_in_bytes = in_bytes;
+    for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);  // keyed by buffer addresses
+    e->graphs.clear();
+  }
+  if (out && !out_pinned && e->stage_out_bytes < out_bytes) {
+    if (e->stage_out) cudaFreeHost(e->stage_out);
+    e->stage_out = nullptr;
+    e->stage_out_bytes = 0;
+    BI_CUDA_TRY(cudaHostAlloc((void**)&e->stage_out, out_bytes, cudaHostAllocPortable));
+    e->stage_out_bytes = out_bytes;
+  }
+  // staged buffers use the device layouts ([Z][n][ldm] / [Z][n][ldi])
+  const double* src = in;
+  int64_t src_ld = ld_in, src_s = s_in;
+  if (in && !in_pinned) {
+    src = e->stage_in;
+    src_ld = e->ldm;
+    src_s = n * e->ldm;
+  }
+  double* dst = out;
+  int64_t dst_ld = ld_out, dst_s = s_out;
+  if (out && !out_pinned) {
+    dst = e->stage_out;
+    dst_ld = e->ldi;
+    dst_s = n * e->ldi;
+  }
+  for (int lv = 0; lv <= e->k; ++lv)
+    if (!e->ev_level[lv]) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_level[lv], cudaEventDisableTiming));
+  for (int z = 0; z < e->Z; ++z)  // fresh M_inv (storage.fresh_state)
+    BI_CUDA_TRY(cudaMemset2DAsync(e->Minv + (int64_t)z * e->si, e->ldi * 8, 0, n * 8, n, s));
+  HostIO io{nullptr, 0, 0, nullptr, 0, 0};
+  std::vector<std::array<int, 4>> blocks;
+  int done = 0;  // last step enqueued
+  for (int lv = 0; lv <= e->k; ++lv) {
+    if (in) {
+      level_blocks(e, lv, blocks);
+      if (!in_pinned) {  // host: user rows -> staging, same coordinates
+        std::vector<Region> regs;
+        for (int z = 0; z < e->Z; ++z)
+          for (const auto& b : blocks) {
+            const int64_t ro = e->off[b[0]], co = e->off[b[2]];
+            regs.push_back({(char*)(e->stage_in + (int64_t)z * src_s + ro * src_ld + co),
+                            (const char*)(in + (int64_t)z * s_in + ro * ld_in + co), src_ld * 8, ld_in * 8,
+                            e->off[b[1]] - ro, (e->off[b[3]] - co) * 8});
+          }
+        par_copy(regs, T);
+      }
+      for (int z = 0; z < e->Z; ++z)
+        for (const auto& b : blocks) {
+          const int64_t ro = e->off[b[0]], co = e->off[b[2]];
+          BI_CUDA_TRY(cudaMemcpy2DAsync(const_cast<double*>(e->M) + (int64_t)z * e->sm + ro * e->ldm + co,
+                                        e->ldm * 8, src + (int64_t)z * src_s + ro * src_ld + co, src_ld * 8,
+                                        (e->off[b[3]] - co) * 8, e->off[b[1]] - ro, cudaMemcpyHostToDevice,
+                                        e->copy_stream));
+        }
+      BI_CUDA_TRY(cudaEventRecord(e->ev_level[lv], e->copy_stream));
+      BI_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_level[lv], 0));
+    } else if (lv < e->k) {
+      continue;  // input already resident: one range
+    }
+    if (done >= last_step) continue;  // stop_after_step: later levels are loaded, not run
+    // steps [2^lv, 2^(lv+1)) first read level lv (Eq. 7); pivot-A reads
+    // everything in its single step
+    int first = done + 1, last;
+    if (e->schedule == BI_SCHEDULE_PIVOT_A) {
+      if (in && lv < e->k) continue;
+      last = 1;
+    } else {
+      last = lv == e->k || !in ? e->nsteps : (1 << (lv + 1)) - 1;
+    }
+    last = std::min(last, last_step);
+    const bool final_range = last == last_step;
+    io.out = final_range ? dst : nullptr;
+    io.ld_out = dst_ld;
+    io.s_out = dst_s;
+    int rc = run_impl(e, first, last, use_graph, s, io.out ? &io : nullptr);
+    if (rc) return rc;
+    done = last;
+  }
+  e->last_first = 1;
+  e->last_last = last_step;
+  if (out && !out_pinned) {  // drain, then staging -> the caller's rows
+    BI_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<Region> regs;
+    for (int z = 0; z < e->Z; ++z)
+      regs.push_back({(char*)(out + (int64_t)z * s_out), (const char*)(dst + (int64_t)z * dst_s), ld_out * 8,
+                      dst_ld * 8, n, n * 8});
+    par_copy(regs, T);
+  }
+  return 0;
+}
+
 extern "C" int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t ld_in, int64_t stride_in,
                                   double* host_out, int64_t ld_out, int64_t stride_out, int first_step,
                                   int last_step, int use_graph, void* stream) {
@@ -1120,6 +1321,15 @@ extern "C" int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t l
   BI_REQUIRE(!host_out || (ld_out >= e->n && (e->Z == 1 || stride_out >= ld_out * e->n)),
              "host output leading dimension / stride too small");
   BI_REQUIRE(!host_in || first_step == 1, "host input requires first_step == 1");
+  const int64_t stage_bytes = (int64_t)e->Z * e->n * std::max(e->ldm, e->ldi) * 8;
+  static const int64_t stage_limit = [] {  // larger pageable buffers: unstaged pageable copies
+    const char* v = getenv("BI_STAGE_LIMIT_GB");
+    return (int64_t)((v ? atof(v) : 8.0) * (1 << 30));
+  }();
+  if (((host_in && !is_pinned(host_in)) || (host_out && !is_pinned(host_out))) && stage_bytes <= stage_limit &&
+      first_step == 1)
+    return run_host_pipelined(e, host_in, ld_in, stride_in, host_out, ld_out, stride_out, last_step, use_graph,
+                              static_cast<cudaStream_t>(stream));
   HostIO io{host_in, ld_in, stride_in, host_out, ld_out, stride_out};
   return run_impl(e, first_step, last_step, use_graph, static_cast<cudaStream_t>(stream), &io);
 }
@@ -1129,7 +1339,11 @@ extern "C" int bi_engine_run_phase(bi_engine* e, int first_step, int last_step, 
   BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step, "stepid outside 1..N_s");
   BI_REQUIRE(mask >= 1 && mask <= 3, "mask must be 1 (GEMM ops), 2 (leaf inversions) or 3");
   e->last_stream = static_cast<cudaStream_t>(stream);
-  BI_CUDA_TRY(enqueue_steps(e, first_step, last_step, e->last_stream, mask));
+  const bool tl = e->timeline;  // timeline events are recorded as graph (external) nodes only
+  e->timeline = false;
+  cudaError_t err = enqueue_steps(e, first_step, last_step, e->last_stream, mask);
+  e->timeline = tl;
+  BI_CUDA_TRY(err);
   return 0;
 }
 

@@ -455,7 +455,9 @@ class ShardedEngine:
 
     def run(self, first: int = 1, last: int | None = None) -> None:
         nsteps = total_steps(self.nb)
-        last = nsteps if last is None else last
+        # the reference always runs at least one step and stops at N_s
+        last = nsteps if last is None else max(first, min(int(last), nsteps))
+        first = max(1, min(first, nsteps))
         if first == 1:
             self.Minv.zero_()
         self._first_fail = None
@@ -491,28 +493,66 @@ class ShardedEngine:
         if v < (1 << 30) * (self.nb + 1):
             raise SingularBlock("A", path=[], step=v // (self.nb + 1), quad=v % (self.nb + 1))
 
-    def gather(self) -> np.ndarray:
-        """The full inverse (collective; every rank receives it)."""
+    def launches(self):
+        """Kernel launches per run (not tracked by the host-driven engine)."""
+        return None
+
+    def write_slab(self, out: np.ndarray) -> None:
+        """Copy this rank's block columns of M_inv into ``out[:, c0:c0+w]``
+        (``out`` is the caller's full n x n host array, shared by the
+        threads of one process)."""
+        if self.w:
+            out[:, self.c0:self.c0 + self.w] = self.Minv.cpu().numpy()
+
+    def _global(self, r: int) -> int:
+        if self.group is self.dist.group.WORLD:
+            return r
+        return self.dist.get_global_rank(self.group, r)
+
+    def gather(self, root: int = 0):
+        """The full inverse on ``root`` (None on the other ranks); collective.
+        Slabs travel one at a time (root receives each into one buffer and
+        writes it into its host array), so no rank ever holds more than its
+        own slab plus one peer slab on the device."""
         import torch
 
         wmax = max(self._width(r) for r in range(self.P))
-        send = torch.zeros((self.n, wmax), dtype=self.Minv.dtype, device=self.Minv.device)
-        send[:, :self.w] = self.Minv
-        recv = self._allgather_tensor(send, self.group, self.P)
-        return torch.cat([recv[r][:, :self._width(r)] for r in range(self.P)], dim=1).cpu().numpy()
+        nccl = self.dist.get_backend(self.group) == "nccl"
+        dev = self.Minv.device if nccl else torch.device("cpu")
+        buf = torch.zeros((self.n, wmax), dtype=self.Minv.dtype, device=dev)
+        out = np.empty((self.n, self.n)) if self.rank == root else None
+        for r in range(self.P):
+            if r == root:
+                if self.rank == root:
+                    self.write_slab(out)
+                continue
+            wr = self._width(r)
+            if self.rank == r:
+                buf[:, :self.w] = self.Minv
+                self.dist.send(buf, dst=self._global(root), group=self.group)
+            elif self.rank == root:
+                self.dist.recv(buf, src=self._global(r), group=self.group)
+                c = self.off[r * self.nbp]
+                out[:, c:c + wr] = buf[:, :wr].cpu().numpy()
+        return out
 
 
-def run_inversion_sharded(m, sizes, group=None, backend=None, stop_after_step=None, dist=None) -> np.ndarray:
+def sharded_engine(sizes, group=None):
+    """This process's rank of the column-sharded engine (one process per GPU,
+    torch.distributed NCCL group)."""
+    return ShardedEngine(sizes, group=group)
+
+
+def run_inversion_sharded(m, sizes, group=None, backend=None, stop_after_step=None, dist=None, root: int = 0):
     """run_inversion (engine.py:482-542) with the matrix column-sharded over the
-    ranks of ``group`` (one process per GPU, or one thread per GPU with a
-    local_group facade as ``dist``).  Every rank passes the same ``m``; every
-    rank receives the full inverse.  Raises SingularBlock like the
-    single-device engine."""
+    ranks of ``group`` (one process per GPU).  Every rank passes the same
+    ``m``; rank ``root`` receives the full inverse, the others None.  Raises
+    SingularBlock like the single-device engine."""
     eng = ShardedEngine(sizes, group=group, backend=backend, dist=dist)
     eng.load(np.asarray(m, dtype=np.float64))
     eng.run(1, stop_after_step)
     eng.check()
-    return eng.gather()
+    return eng.gather(root)
 
 
 def run_inversion_local(m, sizes, gpus: int, stop_after_step=None, devices=None, backend_factory=None) -> np.ndarray:
@@ -528,8 +568,15 @@ def run_inversion_local(m, sizes, gpus: int, stop_after_step=None, devices=None,
 
         _lib.init_devices(sorted(set(devices if devices is not None else range(gpus))))
 
+    out = np.empty(m.shape)
+
     def target(dist, rank):
         be = backend_factory() if backend_factory is not None else None
-        return run_inversion_sharded(m, sizes, backend=be, stop_after_step=stop_after_step, dist=dist)
+        eng = ShardedEngine(sizes, backend=be, dist=dist)
+        eng.load(m)
+        eng.run(1, stop_after_step)
+        eng.check()
+        eng.write_slab(out)  # each thread its own block columns, no all-gather
 
-    return run_threads(gpus, target, devices=devices)[0]
+    run_threads(gpus, target, devices=devices)
+    return out

@@ -15,7 +15,6 @@ GEMM launch covers the whole batch.
 from __future__ import annotations
 
 import os
-import threading
 from collections import OrderedDict
 from dataclasses import dataclass
 
@@ -468,41 +467,25 @@ def _last_step(n_steps: int, stop_after_step) -> int:
     return max(1, min(int(stop_after_step), n_steps))
 
 
-# --- page-locked staging for NumPy (pageable) host buffers -------------------
-# A pageable cudaMemcpy is synchronous and slow; copying through cached
-# page-locked buffers (multi-threaded host copy, then the graph-captured,
-# need-ordered DMA of bi_engine_run_host) is several times faster end to end.
-_STAGE_LIMIT = 4 << 30  # bytes per staging buffer; larger inputs use the pageable path
-_stage_lock = threading.Lock()
-_stage_bufs: dict = {}
-_copy_pool = None
+# --- host buffers -------------------------------------------------------------
+# Pageable NumPy input goes to bi_engine_run_host as is: the engine stages it
+# through its own page-locked buffer in need order, level by level, under
+# the compute (bi_engine.cu run_host_pipelined).  Results up to
+# _PINNED_RESULT_LIMIT bytes are allocated page-locked (torch's caching host
+# allocator; the NumPy result keeps the block alive), so the inverse is
+# DMA'd straight into the caller's array during the last step.
+_PINNED_RESULT_LIMIT = 8 << 30
 
 
-def _pinned_view(which: str, like: np.ndarray) -> np.ndarray:
-    t = _lib.torch()
-    buf = _stage_bufs.get(which)
-    if buf is None or buf.numel() < like.nbytes:
-        _stage_bufs[which] = None
-        buf = _stage_bufs[which] = t.empty(max(like.nbytes, 1), dtype=t.uint8, pin_memory=True)
-    return buf[:like.nbytes].numpy().view(np.float64).reshape(like.shape)
-
-
-def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
-    """dst[...] = src over up to 8 threads (NumPy releases the GIL on large copies)."""
-    global _copy_pool
-    flat_d, flat_s = dst.reshape(-1), src.reshape(-1)
-    n = flat_d.size
-    parts = max(1, min(8, n // (1 << 20)))
-    if parts == 1:
-        np.copyto(flat_d, flat_s)
-        return
-    if _copy_pool is None:
-        from concurrent.futures import ThreadPoolExecutor
-
-        _copy_pool = ThreadPoolExecutor(8, thread_name_prefix="bi-stage")
-    bounds = [n * i // parts for i in range(parts + 1)]
-    list(_copy_pool.map(lambda i: np.copyto(flat_d[bounds[i]:bounds[i + 1]], flat_s[bounds[i]:bounds[i + 1]]),
-                        range(parts)))
+def _result_array(shape) -> np.ndarray:
+    nbytes = 8 * int(np.prod(shape))
+    if nbytes <= _PINNED_RESULT_LIMIT:
+        t = _lib.torch()
+        try:
+            return t.empty(tuple(shape), dtype=t.float64, pin_memory=True).numpy()
+        except RuntimeError:  # page-locked memory exhausted: pageable result
+            pass
+    return np.empty(shape)
 
 
 def _page_locked(a: np.ndarray) -> bool:
@@ -514,18 +497,20 @@ def _page_locked(a: np.ndarray) -> bool:
 
 
 def _run_host_staged(eng, src: np.ndarray, out: np.ndarray, last: int) -> None:
-    """eng.run_host with pageable NumPy buffers, through page-locked staging."""
-    if src.nbytes > _STAGE_LIMIT or not src.flags.c_contiguous or not out.flags.c_contiguous:
-        eng.run_host(src, out, 1, last)
-        eng.check()
-        return
-    with _stage_lock:
-        sin = _pinned_view("in", src)
-        sout = _pinned_view("out", out)
-        _par_copy(sin, src)
-        eng.run_host(sin, sout, 1, last)
-        eng.check()
-        _par_copy(out, sout)
+    """eng.run_host on host buffers (page-locked or pageable; the native
+    engine pipelines pageable input in need order)."""
+    eng.run_host(src, out, 1, last)
+    eng.check()
+
+
+def release_engines() -> None:
+    """Drop the cached device engines (their M, M_inv, T-sets and page-locked
+    staging) -- e.g. before a different large problem."""
+    _ENGINES.clear()
+    t = _lib.torch()
+    if t.cuda.is_available():
+        t.cuda.synchronize()
+        t.cuda.empty_cache()
 
 
 def gpus_for_workers(workers: int | None, nblocks: int) -> int:
@@ -588,15 +573,16 @@ def run_inversion(m, workers: int | None = None, checkpoint_dir=None, file_backe
     if gpus > 1:  # column-sharded over this process's GPUs, one thread per GPU
         from .distributed import run_inversion_local
 
+        last = _last_step(total_steps(len(scheme.sizes)), stop_after_step)
         out = run_inversion_local(np.ascontiguousarray(dense, dtype=np.float64), list(scheme.sizes), gpus,
-                                  stop_after_step=stop_after_step)
+                                  stop_after_step=last)
         if counters is not None:
-            _add_counters(counters, scheme.sizes, _last_step(total_steps(len(scheme.sizes)), stop_after_step))
+            _add_counters(counters, scheme.sizes, last)
         return BlockMatrix(scheme, MemoryBlockStore(scheme, out), role="inverse")
     eng = _engine_for(scheme.sizes, 1, schedule)
     last = _last_step(eng.n_steps, stop_after_step)
     dense = np.ascontiguousarray(dense, dtype=np.float64)
-    out = np.empty((scheme.m_n, scheme.m_n))
+    out = _result_array((scheme.m_n, scheme.m_n))
     _run_host_staged(eng, dense, out, last)
     if counters is not None:
         c = eng.counters(1, last)
@@ -666,12 +652,8 @@ def run_inversion_batch(ms, sizes, out: np.ndarray | None = None,
     eng = _engine_for(scheme.sizes, int(ms_np.shape[0]), schedule)
     last = _last_step(eng.n_steps, stop_after_step)
     if out is None:
-        out = np.empty(ms_np.shape)
-    if _page_locked(ms_np) and _page_locked(out):
-        eng.run_host(ms_np, out, 1, last)  # graph-captured DMA straight from/to the caller's buffers
-        eng.check()
-    else:
-        _run_host_staged(eng, ms_np, out, last)
+        out = _result_array(ms_np.shape)
+    _run_host_staged(eng, ms_np, out, last)
     if counters is not None:
         c = eng.counters(1, last)
         counters.multiplies += c["multiplies"]

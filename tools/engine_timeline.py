@@ -18,7 +18,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_2305_11103_b200 as bi  # noqa: E402
 from paper_2305_11103_b200 import _lib  # noqa: E402
 from paper_2305_11103_b200.engine import decode_step, loopid_for_step  # noqa: E402
-from paper_2305_11103_b200.workloads import cfg2  # noqa: E402
+from paper_2305_11103_b200.workloads import cfg2, cfg4  # noqa: E402
 
 
 def main():
@@ -26,9 +26,15 @@ def main():
     ap.add_argument("--schedule", default="eq7")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--host", action="store_true", help="time the host-buffer path (run_host, pinned)")
+    ap.add_argument("--cfg", type=int, default=2, choices=(2, 4), help="2: batch of 4 x 4096; 4: one 16384")
+    ap.add_argument("--summary", action="store_true", help="per step kind totals instead of every step")
     args = ap.parse_args()
-    ms, sizes = cfg2(4)
-    eng = bi.DeviceEngine(sizes, batch=4, schedule=args.schedule)
+    if args.cfg == 2:
+        ms, sizes = cfg2(4)
+    else:
+        m, sizes = cfg4()
+        ms = m[None]
+    eng = bi.DeviceEngine(sizes, batch=ms.shape[0], schedule=args.schedule)
     eng.load(ms)
     if args.host:
         pin_in = torch.from_numpy(ms).pin_memory()
@@ -39,7 +45,7 @@ def main():
     for _ in range(args.reps):
         run()
     eng.check()
-    nl = min(int(os.environ.get("BI_ENGINE_LANES", "8")), 4)
+    nl = min(int(os.environ.get("BI_ENGINE_LANES", "8")), ms.shape[0])
     ns = eng.n_steps
     buf = (_lib.ctypes.c_float * (nl * (ns + 1)))()
     _lib.check(_lib.lib().bi_engine_timeline(eng._h, buf), "bi_engine_timeline")
@@ -62,6 +68,26 @@ def main():
             kinds.append(f"A{a.sid}")
         else:
             kinds.append(f"D+U{a.depth}")
+    if args.summary:
+        for l in range(nl):
+            tot = {}
+            prev = 0.0
+            for st in range(1, ns + 1):
+                k = kinds[st - 1]
+                c = tot.setdefault(k, [0, 0.0])
+                c[0] += 1
+                c[1] += t[l, st] - prev
+                prev = t[l, st]
+            print(f"L{l}: " + "; ".join(f"{k} x{c[0]} {c[1]:.2f} ms ({c[1] / c[0]:.3f})" for k, c in sorted(tot.items())))
+        for mask, name in ((1, "GEMM ops only"), (2, "leaf inversions only")):
+            for _ in range(2):
+                eng.run_phase(mask)
+            e0.record()
+            eng.run_phase(mask)
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"{name}: {e0.elapsed_time(e1):.2f} ms")
+        return
     print("step " + " ".join(f"{k:>13s}" for k in kinds))
     for l in range(nl):
         row = []
