@@ -145,7 +145,7 @@ def test_cfg5_full_size_one_b200(bi):
     eng.load(m)
     eng.run()
     eng.check()
-    fro, _ = _residual_device(eng.M, eng.Minv)
+    fro, _ = _residual_device(eng.M, eng.Minv, batch=True)
     assert fro[0] <= bound, fro
     num = den = 0.0
     for r0 in range(0, n, 4096):
