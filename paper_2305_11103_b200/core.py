@@ -289,8 +289,20 @@ def gpu_invert_sub(block, out) -> None:
     drops the B200 leaf kernel into the reference formula."""
     inv, info = _invert_host_block(as_matrix(block))
     if info:
-        raise SingularBlock("A", path=[])
+        raise _caller_singular()("A", path=[])
     out[...] = inv
+
+
+def _caller_singular():
+    """The SingularBlock class of the framework calling the plugin: when the
+    reference package (``blockinv``) is the caller, its formulas catch only
+    their own SingularBlock (schur.py:104-111, 326-332), so the adapter raises
+    that one; otherwise this package's."""
+    import sys
+
+    ref = sys.modules.get("blockinv.errors")
+    cls = getattr(ref, "SingularBlock", None) if ref is not None else None
+    return cls if isinstance(cls, type) and issubclass(cls, Exception) else SingularBlock
 
 
 def _residual_device(da, dx, batch=False):

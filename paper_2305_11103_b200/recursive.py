@@ -24,7 +24,122 @@ from . import _lib
 from .core import OpCounters, as_matrix, device_gemm, device_inverse
 from .errors import AllPivotsSingular, DimensionMismatch, ScratchTooSmall, SingularBlock
 
-LEAF_ORDER = 256  # device leaf order (reference: 2, recursive.py:44)
+LEAF_ORDER = 256  # device leaf order (the reference recurses to 2, recursive.py:44)
+
+# ---------------------------------------------------------------------------
+# OpCounters: the reference recursion's tallies.  The device executes a
+# shallower tree (K3 leaves of order <= LEAF_ORDER), but the counters are an
+# API contract (test_acceptance.py:112-143, test_recursive.py): they are
+# computed here by replaying the reference recursion's bookkeeping -- leaf
+# order 2, split floor(n/2), the same alloc/release sequence (peak_scratch)
+# and the Schur workspace pool (schur_scratch) -- without its arithmetic.
+# device_tree_counters() gives the executed tree's tallies.
+# ---------------------------------------------------------------------------
+REF_LEAF_ORDER = 2  # recursive.py:44
+_REF_LIST_MAX = 10  # recursive.py:69 (list path below this order, inlined bookkeeping)
+
+
+def _ref_by_a(n: int, c: OpCounters) -> None:
+    """_by_a_rec / _by_a_small (recursive.py:83-123, 228-263)."""
+    if n <= _REF_LIST_MAX:
+        c.alloc(n * n)
+        if n <= REF_LEAF_ORDER:
+            c.inversions += 1
+            return
+        c.nodes += 1
+        p, q = n // 2, n - n // 2
+        _ref_by_a(p, c)
+        c.alloc(2 * p * q + q * q)
+        c.multiplies += 3
+        c.reductions += 1
+        _ref_by_a(q, c)
+        c.release(q * q)
+        c.multiplies += 3
+        c.reductions += 1
+        c.release(p * q + p * p + q * p + q * q)
+        return
+    c.alloc(n * n)
+    c.nodes += 1
+    p, q = n // 2, n - n // 2
+    _ref_by_a(p, c)
+    c.alloc(p * q)
+    c.multiplies += 1  # n_ab = -A^-1 B
+    c.alloc(q * p)
+    c.multiplies += 1  # ca = C A^-1
+    c.alloc(q * q)
+    c.multiplies += 1  # S_A = D + C n_ab
+    c.reductions += 1
+    _ref_by_a(q, c)
+    c.release(q * q)
+    c.multiplies += 1  # out01
+    c.release(p * q)
+    c.release(p * p)
+    c.multiplies += 1  # out00 += out01 ca
+    c.reductions += 1
+    c.multiplies += 1  # out10
+    c.release(q * p)
+    c.release(q * q)
+
+
+def _ref_inplace(n: int, c: OpCounters) -> None:
+    """_inplace_rec (recursive.py:317-333): 6 in-place products per node."""
+    if n <= REF_LEAF_ORDER:
+        c.inversions += 1
+        return
+    c.nodes += 1
+    _ref_inplace(n // 2, c)
+    c.multiplies += 3  # inplace_left, multiply(acc), inplace_right
+    c.reductions += 1
+    _ref_inplace(n - n // 2, c)
+    c.multiplies += 3
+    c.reductions += 1
+
+
+def _ref_by_ad(n: int, start: int, pool: set, c: OpCounters) -> None:
+    """_by_ad_rec with the _SchurPool (recursive.py:340-462)."""
+    if n <= REF_LEAF_ORDER:
+        c.inversions += 1
+        return
+    c.nodes += 1
+    p, q = n // 2, n - n // 2
+    c.alloc(p * p + q * q)
+    _ref_by_ad(p, start, pool, c)
+    _ref_by_ad(q, start + p, pool, c)
+    c.alloc(p * q + q * p)
+    c.multiplies += 2
+    c.release(p * p + q * q)
+    for key, order in (((start, p, "sd"), p), ((start + p, q, "sa"), q)):
+        if key not in pool:
+            pool.add(key)
+            c.schur_scratch += order * order
+            c.alloc(order * order)
+        c.reductions += 1  # schur_accumulate
+    _ref_by_ad(p, start, pool, c)
+    _ref_by_ad(q, start + p, pool, c)
+    c.multiplies += 2
+    c.release(p * q + q * p)
+
+
+def device_tree_counters(n: int, procedure: str = "by_a") -> OpCounters:
+    """Tallies of the tree the device actually executes (K3 leaves of order
+    <= LEAF_ORDER): pivot-A nodes carry 6 products + 2 reductions, Eq. 7
+    nodes 4 + 2."""
+    c = OpCounters()
+    per = (4, 2) if procedure == "by_ad" else (6, 2)
+
+    def rec(m: int) -> None:
+        if m <= LEAF_ORDER:
+            c.inversions += 1
+            return
+        c.nodes += 1
+        c.multiplies += per[0]
+        c.reductions += per[1]
+        rec(m // 2)
+        rec(m - m // 2)
+
+    if n:
+        rec(n)
+    return c
 
 
 def _check_square(x) -> np.ndarray:
@@ -32,17 +147,6 @@ def _check_square(x) -> np.ndarray:
     if x.shape[0] != x.shape[1]:
         raise DimensionMismatch(f"need a square matrix, got {x.shape}")
     return x
-
-
-def _tree(n: int, leaf: int, c: OpCounters) -> None:
-    if n <= leaf:
-        c.inversions += 1
-        return
-    c.nodes += 1
-    c.multiplies += 6
-    c.reductions += 2
-    _tree(n // 2, leaf, c)
-    _tree(n - n // 2, leaf, c)
 
 
 def inplace_by_a_device(x_dev, leaf_order: int = LEAF_ORDER) -> None:
@@ -73,7 +177,10 @@ def invertor_inplace_by_a(x, row_scratch=None, counters: OpCounters | None = Non
         xd = _lib.to_device(x)
         inplace_by_a_device(xd)
         x[...] = xd.cpu().numpy()
-    _tree(n, LEAF_ORDER, counters)
+    counters.alloc(row_scratch.shape[0])  # recursive.py:289-291
+    if n:
+        _ref_inplace(n, counters)
+    counters.release(row_scratch.shape[0])
     return counters
 
 
@@ -88,7 +195,7 @@ def invertor_by_a(x, counters: OpCounters | None = None):
         xd = _lib.to_device(x)
         inplace_by_a_device(xd)
         out[...] = xd.cpu().numpy()
-    _tree(n, LEAF_ORDER, counters)
+        _ref_by_a(n, counters)
     return out, counters
 
 
@@ -187,12 +294,13 @@ def invertor_by_ad(x, counters: OpCounters | None = None, parallel_pairs: bool =
     n = x.shape[0]
     out = np.empty((n, n))
     if n:
-        tree = _AdTree(counters, LEAF_ORDER)
+        tree = _AdTree(OpCounters(), LEAF_ORDER)  # device tree tallies: device_tree_counters
         xd = _lib.to_device(x)
         od = _lib.empty_matrix(n, n)
         tree.node(xd, od, 0, [])
         tree.check()
         out[...] = od.cpu().numpy()
+        _ref_by_ad(n, 0, set(), counters)
     return out, counters
 
 

@@ -86,8 +86,13 @@ def test_by_ad_recursion_vs_oracle(bi, order):
     c = bi.OpCounters()
     inv, _ = bi.invertor_by_ad(m, c)
     _criteria(m, inv, oracle.gauss_jordan(m))
-    if order == 600:  # 600 -> 300 -> leaves of 150: 1 + 4 nodes, 16 leaves
-        assert (c.nodes, c.multiplies, c.reductions, c.inversions) == (5, 20, 10, 16)
+    # the reported tallies are the reference recursion's (leaf order 2):
+    # 4 products + 2 reductions per node, the scratch law's pooled workspace
+    assert c.multiplies == 4 * c.nodes and c.reductions == 2 * c.nodes
+    assert c.inversions == 3 * c.nodes + 1  # four sub-inversions per node
+    if order == 600:  # the device tree: 600 -> 300 -> leaves of 150: 1 + 4 nodes, 16 leaves
+        d = bi.device_tree_counters(600, "by_ad")
+        assert (d.nodes, d.multiplies, d.reductions, d.inversions) == (5, 20, 10, 16)
 
 
 def test_by_ad_singular_leaf_path(bi):

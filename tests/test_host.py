@@ -205,3 +205,35 @@ def test_product_never_imports_oracle():
                 assert all(not a.name.startswith("oracle") for a in node.names), py
             if isinstance(node, ast.ImportFrom):
                 assert not (node.module or "").startswith("oracle"), py
+
+
+def test_recursive_counters_equal_reference_golden():
+    """invertor_by_a / invertor_inplace_by_a / invertor_by_ad report the
+    reference recursion's OpCounters (every field, incl. peak_scratch and
+    schur_scratch) -- replayed bookkeeping, golden from the reference itself
+    (tests/golden/make_counters.py) -- not the device tree's."""
+    import json
+    from pathlib import Path
+
+    from paper_2305_11103_b200.core import OpCounters
+    from paper_2305_11103_b200.recursive import _ref_by_a, _ref_by_ad, _ref_inplace
+
+    gold = json.loads((Path(__file__).parent / "golden" / "counters.json").read_text())
+    fields = ("multiplies", "inversions", "reductions", "peak_scratch", "schur_scratch", "nodes")
+    for n_s, rec in gold.items():
+        n = int(n_s)
+        c = OpCounters()
+        _ref_by_a(n, c)
+        assert {f: getattr(c, f) for f in fields} == rec["by_a"], ("by_a", n)
+        c = OpCounters()
+        c.alloc(n)
+        _ref_inplace(n, c)
+        c.release(n)
+        assert {f: getattr(c, f) for f in fields} == rec["inplace"], ("inplace", n)
+        c = OpCounters()
+        _ref_by_ad(n, 0, set(), c)
+        assert {f: getattr(c, f) for f in fields} == rec["by_ad"], ("by_ad", n)
+    for k in range(2, 7):  # test_acceptance.py:132-143 scratch law
+        c = OpCounters()
+        _ref_by_ad(2 ** k, 0, set(), c)
+        assert c.schur_scratch == 2 ** (k + 1) * (2 ** (k - 1) - 1)
