@@ -134,8 +134,9 @@ def device_tree_counters(n: int, procedure: str = "by_a") -> OpCounters:
         c.nodes += 1
         c.multiplies += per[0]
         c.reductions += per[1]
-        rec(m // 2)
-        rec(m - m // 2)
+        for _ in range(2 if procedure == "by_ad" else 1):  # Eq. 7: A, D then S_D, S_A
+            rec(m // 2)
+            rec(m - m // 2)
 
     if n:
         rec(n)

@@ -68,6 +68,7 @@ def run() -> None:
     env = dict(os.environ)
     env["PYTHONPATH"] = os.pathsep.join([str(ROOT / "tools" / "refshim"), str(ROOT)])
     cmd = [sys.executable, "-m", "pytest", str(DEST / "tests"), "-q", "-rfE", "-p", "no:cacheprovider",
+           "--continue-on-collection-errors",
            "--rootdir", str(DEST / "tests"), "-o", "addopts="]
     r = subprocess.run(cmd, cwd=str(DEST / "tests"), env=env, capture_output=True, text=True)
     env2 = dict(os.environ)
