@@ -180,6 +180,47 @@ int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t ld_in, int64
                        double* host_out, int64_t ld_out, int64_t stride_out,
                        int first_step, int last_step, int use_graph, void* stream);
 int bi_engine_status(bi_engine* e, int* fail_step, int* fail_quad, int* fail_matrix);
+
+/* ------------------------------------------------------------------------
+ * Column-sharded level scheduler: the engine of rank `rank` of
+ * `nranks` (a power of two dividing nblocks; batch 1, Eq. 7).  Rank r owns
+ * the home range of diagonal blocks [r N_b/P, (r+1) N_b/P) and stores block
+ * COLUMNS of that range of M, M_inv and every T_l (bind M / M_inv as n x w
+ * slabs).  Local levels (2^l <= N_b/P) run without communication; each
+ * global-level action starts with an exchange inside its rank group
+ * (engine.py:336-437 split by output columns, K never split, so every P is
+ * bitwise equal to P = 1):
+ *   arrows   A-half ranks send [A^-1 ; C], D-half ranks [B ; D^-1]
+ *            (the inverted pivot blocks and the off-diagonal operands);
+ *   up/down  A-half ranks share L, D-half ranks R.
+ * The replaced reference interface is the engine's fork-join over workers
+ * (engine.py:257-285) and INVERTOR_WORKERS (engine.py:58-65).
+ *
+ *   bi_engine_shard_segments -> the op ranges between exchanges of steps
+ *        [first, last]: begin/end into the flat op list, xchg = the exchange
+ *        after the segment (-1 none); returns the count (call with cap 0 to size).
+ *   bi_engine_run_ops        -> enqueue one segment (graph-captured).
+ *   Transport A, all ranks in one process (one GPU each; tests may map
+ *   several ranks to one GPU): bi_shard_group_run drives every rank from
+ *   one host thread -- peer copies (NVLink, P2P enabled by bi_init) of the
+ *   members' send windows into each reader's X, ordered by events.
+ *   Transport B, one process per GPU: create with BI_SHARD_STAGING, then per
+ *   exchange bi_engine_xchg_pack (send parts -> send area, rows x wmax),
+ *   an all-gather of the send areas inside the group (NCCL) into the receive
+ *   area ([gs][rows][wmax]), bi_engine_xchg_unpack (-> X).
+ * ---------------------------------------------------------------------- */
+#define BI_SHARD_STAGING 1
+int bi_engine_create_shard(bi_engine** out, int nblocks, const int64_t* sizes, int nranks, int rank, int flags);
+int bi_engine_shard_info(const bi_engine* e, int64_t out[8]);   /* P, rank, col0, w, wmax, #xchg, send, recv elems */
+int bi_engine_shard_segments(const bi_engine* e, int first_step, int last_step, int* begin, int* end, int* xchg,
+                             int cap);
+int bi_engine_run_ops(bi_engine* e, int op_begin, int op_end, int use_graph, void* stream);
+int bi_engine_xchg_desc(const bi_engine* e, int i, int64_t out[8]); /* g0, gs, rows, wmax, in_a, from0, from1, kind*100+level */
+int bi_engine_shard_buffers(const bi_engine* e, double** sendbuf, double** recvbuf);
+int bi_engine_xchg_pack(bi_engine* e, int i, void* stream);
+int bi_engine_xchg_unpack(bi_engine* e, int i, void* stream);
+int bi_shard_group_run(bi_engine** engines, int nranks, void* const* streams, int first_step, int last_step,
+                       int use_graph);
 /* Enqueue only one class of ops of steps [first, last] (no graph): mask 1 =
  * the engine's K1 GEMM launches, 2 = the leaf inversions (K3 incl. their
  * trailing-update GEMMs), 3 = both.  For per-kernel timing in bench.py. */

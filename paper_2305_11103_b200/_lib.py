@@ -55,6 +55,16 @@ SIGNATURES = [
     ("bi_engine_tset_square", _c_int, [_vp, _c_int, _c_int, _c_int, ctypes.POINTER(_vp),
                                        ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)]),
     ("bi_engine_destroy", _c_int, [_vp]),
+    ("bi_engine_create_shard", _c_int, [ctypes.POINTER(_vp), _c_int, ctypes.POINTER(_c_i64), _c_int, _c_int,
+                                        _c_int]),
+    ("bi_engine_shard_info", _c_int, [_vp, ctypes.POINTER(_c_i64)]),
+    ("bi_engine_shard_segments", _c_int, [_vp, _c_int, _c_int, _pint, _pint, _pint, _c_int]),
+    ("bi_engine_run_ops", _c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
+    ("bi_engine_xchg_desc", _c_int, [_vp, _c_int, ctypes.POINTER(_c_i64)]),
+    ("bi_engine_shard_buffers", _c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    ("bi_engine_xchg_pack", _c_int, [_vp, _c_int, _vp]),
+    ("bi_engine_xchg_unpack", _c_int, [_vp, _c_int, _vp]),
+    ("bi_shard_group_run", _c_int, [ctypes.POINTER(_vp), _c_int, ctypes.POINTER(_vp), _c_int, _c_int, _c_int]),
     ("bi_schur2x2_workspace_bytes", _c_i64, [_c_i64, _c_i64]),
     ("bi_schur2x2", _c_int, [_c_int, _c_i64, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _pint, _vp]),
     ("bi_inplace_by_a_workspace_bytes", _c_i64, [_c_i64, _c_i64]),

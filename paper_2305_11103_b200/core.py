@@ -181,6 +181,24 @@ def device_inverse_list(blocks, outs):
 # ---------------------------------------------------------------------------
 
 
+# core.py:110-112: the reference dispatches small products to a Python loop
+# below this many multiply-adds; on the device every product is K1, so the
+# threshold changes nothing (kept for callers that tune it).
+_SMALL_PRODUCT = 512
+_SMALL_EDGE = 8
+
+
+def _mm_acc(a, b, out, negate: bool = False) -> None:
+    """out += (+-1) a @ b (core.py:115-139): the GEMM primitive every
+    product of the reference goes through, here one K1 launch (C = out)."""
+    if a.shape[1] != b.shape[0] or out.shape != (a.shape[0], b.shape[1]):
+        raise DimensionMismatch(f"_mm_acc {a.shape} x {b.shape} -> {out.shape}")
+    if out.size and a.shape[1]:
+        dout = _lib.to_device(out)
+        device_gemm(_lib.to_device(a), _lib.to_device(b), dout, c=dout, negate=negate)
+        out[...] = dout.cpu().numpy()
+
+
 def multiply(a, b, out, accumulate=False, negate=False, counters: OpCounters | None = None) -> None:
     """out = (+-1) a @ b, or out += ... when ``accumulate`` (core.py:142-170)."""
     if a.shape[1] != b.shape[0] or out.shape[0] != a.shape[0] or out.shape[1] != b.shape[1]:

@@ -176,6 +176,9 @@ struct bi_engine {
   // layout
   struct Sq {
     int64_t off, side, ld;
+    int64_t col_origin;  // matrix column of the square's column 0 (the quad's first column, or
+                         // this rank's first column for a column-sharded global-level quad)
+    bool present;        // false: the quad holds none of this rank's columns
   };
   std::vector<std::vector<Sq>> tsq;  // [level][quad]
   int64_t t_matrix = 0;              // elements per matrix (all levels)
@@ -201,6 +204,39 @@ struct bi_engine {
     gemm_cap = pol[i].gemm_cap;
   }
   int zlo[kMaxLanes] = {}, zhi[kMaxLanes] = {};
+  // ---- column-sharded rank of a P-GPU run (bi_engine_create_shard).
+  // P == 1: the whole matrix.  Rank r owns block columns [h0, h1) of M, M_inv
+  // and every T_l; local levels (2^l <= N_b/P) need nothing from other ranks,
+  // a global-level action first assembles its replicated operand X from the
+  // group's column slabs (an "exchange"), then runs on this rank's columns.
+  int P = 1, rank = 0, nbp = 0, h0 = 0, h1 = 0;
+  int64_t col0 = 0, w = 0, wmax = 0;  // first owned column, owned width, widest rank
+  int shard_flags = 0;
+  struct Xchg {
+    int level = 0, kind = 0;       // kind 0: arrows ([A^-1; C] / [B; D^-1]), 1: up/down pass (L / R)
+    int g0 = 0, gs = 0;            // group: ranks [g0, g0 + gs)
+    bool in_a = false;             // this rank's columns lie in the quad's A half
+    const double* top = nullptr;   // this rank's send parts: rows x w windows
+    int64_t top_ld = 0, top_rows = 0;
+    const double* bot = nullptr;
+    int64_t bot_ld = 0, bot_rows = 0;
+    int from0 = 0, from1 = 0;      // ranks whose send parts form X (columns side by side)
+    int64_t x_col0 = 0;            // matrix column of X's column 0
+    int64_t rows = 0, xcols = 0, ldx = 0;
+  };
+  std::vector<Xchg> xchgs;
+  int64_t x_elems = 0, send_elems = 0, recv_elems = 0;
+  double* X = nullptr;
+  double* sendbuf = nullptr;
+  double* recvbuf = nullptr;
+  struct FlatOp {
+    int stepid;
+    Op op;  // kind 3: exchange (index into xchgs)
+  };
+  std::vector<FlatOp> flat;         // lane 0's ops of steps 1..N_s in order
+  std::vector<int> step_first_op;   // [stepid] -> first index into flat (N_s + 2 entries)
+  std::map<std::pair<int, int>, cudaGraphExec_t> seg_graphs;
+  int device = 0;
   int* info = nullptr;
   GemmDesc* d_descs = nullptr;
   void* d_ptrs = nullptr;
@@ -239,6 +275,7 @@ struct bi_engine {
   cudaEvent_t ev_level[32] = {};  // H2D of input level l done (pipelined host path)
 
   ~bi_engine() {
+    for (auto& kv : seg_graphs) cudaGraphExecDestroy(kv.second);
     if (stage_in) cudaFreeHost(stage_in);
     if (stage_out) cudaFreeHost(stage_out);
     for (cudaEvent_t ev : ev_level)
@@ -273,14 +310,16 @@ struct bi_engine {
     double* base = T + (int64_t)z * t_matrix + s.off;
     (void)r1;
     (void)c1;
-    return Window{base + (off[r0] - origin) * s.ld + (off[c0] - origin), s.ld};
+    return Window{base + (off[r0] - origin) * s.ld + (off[c0] - s.col_origin), s.ld};
   }
+  // M and M_inv hold this rank's columns [col0, col0 + w) (all of them for P = 1)
   Window m_window(int z, int r0, int c0) const {
-    return Window{const_cast<double*>(M) + (int64_t)z * sm + off[r0] * ldm + off[c0], ldm};
+    return Window{const_cast<double*>(M) + (int64_t)z * sm + off[r0] * ldm + (off[c0] - col0), ldm};
   }
   Window minv_window(int z, int r0, int c0) const {
-    return Window{Minv + (int64_t)z * si + off[r0] * ldi + off[c0], ldi};
+    return Window{Minv + (int64_t)z * si + off[r0] * ldi + (off[c0] - col0), ldi};
   }
+  bool is_global(int level) const { return (1 << level) > nbp; }
   Window source(const StepAct& a, int z, int r0, int r1, int c0, int c1) const {
     return a.from_tset ? tset_window(a.cid, z, r0, r1, c0, c1) : m_window(z, r0, c0);
   }
@@ -305,7 +344,8 @@ static void pivot_a_footprint(const std::vector<int64_t>& off, int b0, int b1, i
   pivot_a_footprint(off, mid, b1, depth + 1, per_depth);
 }
 
-extern "C" int bi_engine_create_ex(bi_engine** out, int nblocks, const int64_t* sizes, int batch, int schedule) {
+static int create_common(bi_engine** out, int nblocks, const int64_t* sizes, int batch, int schedule, int nranks,
+                         int rank, int flags) {
   BI_REQUIRE(out != nullptr && sizes != nullptr, "null argument");
   BI_REQUIRE(schedule == BI_SCHEDULE_EQ7 || schedule == BI_SCHEDULE_PIVOT_A, "unknown schedule");
   BI_REQUIRE(nblocks >= 1 && (nblocks & (nblocks - 1)) == 0,
@@ -327,18 +367,53 @@ extern "C" int bi_engine_create_ex(bi_engine** out, int nblocks, const int64_t* 
   }
   (void)maxb;  // blocks above kInvMaxDirect invert by a pivot-A recursion with K3 leaves
   e->n = e->off.back();
-  // T-set layout (per matrix)
+  BI_REQUIRE(nranks >= 1 && (nranks & (nranks - 1)) == 0 && nblocks % nranks == 0 && rank >= 0 && rank < nranks,
+             "the rank count must be a power of two dividing the number of diagonal blocks");
+  e->P = nranks;
+  e->rank = rank;
+  e->shard_flags = flags;
+  e->nbp = nblocks / nranks;
+  e->h0 = rank * e->nbp;
+  e->h1 = e->h0 + e->nbp;
+  e->col0 = e->off[e->h0];
+  e->w = e->off[e->h1] - e->col0;
+  for (int r = 0; r < nranks; ++r)
+    e->wmax = std::max(e->wmax, e->off[(size_t)(r + 1) * e->nbp] - e->off[(size_t)r * e->nbp]);
+  // T-set layout (per matrix): every level-l quad holding some of this rank's
+  // columns; a quad wider than the home range keeps only the home columns
   e->tsq.resize(e->k + 1);
   int64_t t = 0;
   for (int lv = 1; lv <= e->k; ++lv) {
     const int nq = nblocks >> lv;
     for (int g = 0; g < nq; ++g) {
-      const int64_t side = e->off[(size_t)(g + 1) << lv] - e->off[(size_t)g << lv];
-      const int64_t ld = round_up(side, 4);
-      e->tsq[lv].push_back({t, side, ld});
+      const int first = g << lv, last = (g + 1) << lv;
+      const int64_t side = e->off[last] - e->off[first];
+      if (last <= e->h0 || first >= e->h1) {
+        e->tsq[lv].push_back({-1, side, 0, 0, false});
+        continue;
+      }
+      const int c_lo = std::max(first, e->h0), c_hi = std::min(last, e->h1);
+      const int64_t cols = e->off[c_hi] - e->off[c_lo];
+      const int64_t ld = round_up(cols, 4);
+      e->tsq[lv].push_back({t, side, ld, e->off[c_lo], true});
       t += round_up(side * ld, 32);
     }
   }
+  // global-level exchange buffers: X (the replicated operand of one action)
+  // and, with BI_SHARD_STAGING, contiguous send / all-gather receive areas
+  for (int lv = 1; lv <= e->k; ++lv) {
+    if ((1 << lv) <= e->nbp) continue;
+    const int g = e->h0 >> lv, first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+    const int64_t ha = e->off[mid] - e->off[first], hd = e->off[last] - e->off[mid];
+    const bool in_a = e->h1 <= mid;
+    const int gs = (1 << lv) / e->nbp;
+    const int64_t xa = (ha + hd) * round_up(in_a ? hd : ha, 4);           // arrows
+    const int64_t xu = in_a ? hd * round_up(ha, 4) : ha * round_up(hd, 4);  // up/down pass
+    e->x_elems = std::max(e->x_elems, std::max(xa, xu));
+    e->send_elems = std::max(e->send_elems, (ha + hd) * e->wmax);
+    e->recv_elems = std::max(e->recv_elems, (int64_t)gs * (ha + hd) * e->wmax);
+  }
+  if (!(flags & BI_SHARD_STAGING)) e->send_elems = e->recv_elems = 0;
   if (schedule == BI_SCHEDULE_PIVOT_A) {  // no T-sets: per-depth T_b / T_c temporaries instead
     std::vector<int64_t> per_depth;
     pivot_a_footprint(e->off, 0, nblocks, 0, per_depth);
@@ -366,7 +441,8 @@ extern "C" int bi_engine_create_ex(bi_engine** out, int nblocks, const int64_t* 
   std::map<int64_t, int> cnt;
   int lane_max = 0;
   for (int l = 0; l < e->nlanes; ++l) lane_max = std::max(lane_max, e->zhi[l] - e->zlo[l]);
-  for (int64_t s : e->sizes) {
+  for (int p = e->h0; p < e->h1; ++p) {
+    const int64_t s = e->sizes[p];
     if (schedule == BI_SCHEDULE_PIVOT_A) cnt[s] = lane_max;  // one leaf at a time per lane
     else cnt[s] += lane_max;
   }
@@ -380,10 +456,20 @@ extern "C" int bi_engine_create_ex(bi_engine** out, int nblocks, const int64_t* 
   return 0;
 }
 
+extern "C" int bi_engine_create_ex(bi_engine** out, int nblocks, const int64_t* sizes, int batch, int schedule) {
+  return create_common(out, nblocks, sizes, batch, schedule, 1, 0, 0);
+}
+
+extern "C" int bi_engine_create_shard(bi_engine** out, int nblocks, const int64_t* sizes, int nranks, int rank,
+                                      int flags) {
+  return create_common(out, nblocks, sizes, 1, BI_SCHEDULE_EQ7, nranks, rank, flags);
+}
+
 extern "C" int64_t bi_engine_workspace_bytes(const bi_engine* e) {
   if (!e) return -1;
   // schedule metadata (descriptor and pointer tables) is engine-owned device memory
-  return e->t_bytes + e->nlanes * e->inv_scratch + align256(e->info_ints * 4);
+  return e->t_bytes + e->nlanes * e->inv_scratch + align256(e->info_ints * 4) + align256(e->x_elems * 8) +
+         align256(e->send_elems * 8) + align256(e->recv_elems * 8);
 }
 
 static int build_pivot_a(bi_engine* e);
@@ -425,6 +511,63 @@ static int build_schedule(bi_engine* e) {
     g.skip_len = 0;
     return g;
   };
+  e->xchgs.clear();
+  // one global-level exchange of this rank (its group, send parts, X layout)
+  auto add_xchg = [&](int lv, int kind, const StepAct& a) -> int {
+    bi_engine::Xchg x;
+    x.level = lv;
+    x.kind = kind;
+    const int g = e->h0 >> lv, first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+    const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
+    x.gs = (1 << lv) / e->nbp;
+    x.g0 = e->rank / x.gs * x.gs;
+    x.in_a = e->h1 <= mid;
+    const int half = x.gs / 2;
+    auto part = [](Window wdw, const double*& p, int64_t& ld) {
+      p = wdw.p;
+      ld = wdw.ld;
+    };
+    if (kind == 0) {  // arrows: A-half ranks send [A^-1 ; C], D-half ranks [B ; D^-1]; X = the other half's
+      if (x.in_a) {
+        part(e->minv_window(0, first, e->h0), x.top, x.top_ld);
+        part(e->source(a, 0, mid, last, e->h0, e->h1), x.bot, x.bot_ld);
+        x.from0 = x.g0 + half;
+        x.from1 = x.g0 + x.gs;
+        x.x_col0 = off[mid];
+        x.xcols = hd;
+      } else {
+        part(e->source(a, 0, first, mid, e->h0, e->h1), x.top, x.top_ld);
+        part(e->minv_window(0, mid, e->h0), x.bot, x.bot_ld);
+        x.from0 = x.g0;
+        x.from1 = x.g0 + half;
+        x.x_col0 = off[first];
+        x.xcols = ha;
+      }
+      x.top_rows = ha;
+      x.bot_rows = hd;
+      x.rows = ha + hd;
+    } else {  // up/down pass: A-half ranks share their L columns, D-half ranks their R columns
+      if (x.in_a) {
+        part(e->tset_window(lv, 0, mid, last, e->h0, e->h1), x.top, x.top_ld);
+        x.top_rows = hd;
+        x.from0 = x.g0;
+        x.from1 = x.g0 + half;
+        x.x_col0 = off[first];
+        x.xcols = ha;
+      } else {
+        part(e->tset_window(lv, 0, first, mid, e->h0, e->h1), x.top, x.top_ld);
+        x.top_rows = ha;
+        x.from0 = x.g0 + half;
+        x.from1 = x.g0 + x.gs;
+        x.x_col0 = off[mid];
+        x.xcols = hd;
+      }
+      x.rows = x.top_rows;
+    }
+    x.ldx = round_up(x.xcols, 4);
+    e->xchgs.push_back(x);
+    return (int)e->xchgs.size() - 1;
+  };
   int info_cursor = 0;
   for (int stepid = 1; stepid <= e->nsteps; ++stepid) {
     StepAct a;
@@ -442,7 +585,7 @@ static int build_schedule(bi_engine* e) {
       // diag: group leaves (z, p) by block size
       std::map<int64_t, std::vector<std::pair<int, int>>> groups;
       for (int z = Z0; z < Z1; ++z)
-        for (int p = 0; p < nb; ++p) groups[e->sizes[p]].push_back({z, p});
+        for (int p = e->h0; p < e->h1; ++p) groups[e->sizes[p]].push_back({z, p});
       for (auto& kv : groups) {
         InvRec r{};
         r.g.n = (int)kv.first;
@@ -461,9 +604,26 @@ static int build_schedule(bi_engine* e) {
       ++diag_index;
       if (a.kind == 2) {
         for (int lv = 1; lv <= a.depth; ++lv) {
+          if (e->is_global(lv)) {  // exchange L / R inside the group, then this rank's columns
+            const int xi = add_xchg(lv, 1, a);
+            const auto& x = e->xchgs[xi];
+            const int g = e->h0 >> lv, first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+            const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
+            const Window X{e->X, x.ldx};
+            std::vector<GemmDesc> raw;
+            if (x.in_a)  // Minv[D, my A cols] = L Minv[A, my A cols]
+              raw.push_back(gemm(X, e->minv_window(0, first, e->h0), nullptr, 0, e->minv_window(0, mid, e->h0), hd,
+                                 e->w, ha, 0));
+            else  // Minv[A, my D cols] = R Minv[D, my D cols]
+              raw.push_back(gemm(X, e->minv_window(0, mid, e->h0), nullptr, 0, e->minv_window(0, first, e->h0), ha,
+                                 e->w, hd, 0));
+            ops.push_back({3, xi});
+            ops.push_back({1, add_launch(raw)});
+            continue;
+          }
           std::vector<GemmDesc> raw;
           for (int z = Z0; z < Z1; ++z)
-            for (int g = 0; g < (nb >> lv); ++g) {
+            for (int g = (e->h0 >> lv); g < (e->h1 >> lv); ++g) {
               const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
               const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
               // down: Minv[D, A] = L * Minv[A, A]
@@ -471,7 +631,7 @@ static int build_schedule(bi_engine* e) {
                                  nullptr, 0, e->minv_window(z, mid, first), hd, ha, ha, 0));
             }
           for (int z = Z0; z < Z1; ++z)
-            for (int g = 0; g < (nb >> lv); ++g) {
+            for (int g = (e->h0 >> lv); g < (e->h1 >> lv); ++g) {
               const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
               const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
               // up: Minv[A, D] = R * Minv[D, D]
@@ -481,12 +641,38 @@ static int build_schedule(bi_engine* e) {
           ops.push_back({1, add_launch(raw)});
         }
       }
+    } else if (e->is_global(a.sid)) {
+      // global arrows: X = the other half's [B ; D^-1] (A-half ranks) or
+      // [A^-1 ; C] (D-half ranks); then this rank's columns of L, S_D / R, S_A
+      const int lv = a.sid;
+      const int xi = add_xchg(lv, 0, a);
+      const auto& x = e->xchgs[xi];
+      const int g = e->h0 >> lv, first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
+      const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
+      const Window X0{e->X, x.ldx}, X1{e->X + ha * x.ldx, x.ldx};
+      std::vector<GemmDesc> l1, l2;
+      if (x.in_a) {
+        const Window Lm = e->tset_window(lv, 0, mid, last, e->h0, e->h1);
+        l1.push_back(gemm(X1, e->source(a, 0, mid, last, e->h0, e->h1), nullptr, 0, Lm, hd, e->w, hd, 1));  // -D^-1 C
+        const Window Am = e->source(a, 0, first, mid, e->h0, e->h1);
+        l2.push_back(gemm(X0, Lm, Am.p, Am.ld, e->tset_window(lv, 0, first, mid, e->h0, e->h1), ha, e->w, hd,
+                          0));  // S_D = A + B L
+      } else {
+        const Window Rm = e->tset_window(lv, 0, first, mid, e->h0, e->h1);
+        l1.push_back(gemm(X0, e->source(a, 0, first, mid, e->h0, e->h1), nullptr, 0, Rm, ha, e->w, ha, 1));  // -A^-1 B
+        const Window Dm = e->source(a, 0, mid, last, e->h0, e->h1);
+        l2.push_back(gemm(X1, Rm, Dm.p, Dm.ld, e->tset_window(lv, 0, mid, last, e->h0, e->h1), hd, e->w, ha,
+                          0));  // S_A = D + C R
+      }
+      ops.push_back({3, xi});
+      ops.push_back({1, add_launch(l1)});
+      ops.push_back({1, add_launch(l2)});
     } else {
       const int lv = a.sid;
       std::vector<GemmDesc> l1, l2;
       for (int kind = 0; kind < 2; ++kind)
         for (int z = Z0; z < Z1; ++z)
-          for (int g = 0; g < (nb >> lv); ++g) {
+          for (int g = (e->h0 >> lv); g < (e->h1 >> lv); ++g) {
             const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
             const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
             Window B = e->source(a, z, first, mid, mid, last);
@@ -501,7 +687,7 @@ static int build_schedule(bi_engine* e) {
           }
       for (int kind = 0; kind < 2; ++kind)
         for (int z = Z0; z < Z1; ++z)
-          for (int g = 0; g < (nb >> lv); ++g) {
+          for (int g = (e->h0 >> lv); g < (e->h1 >> lv); ++g) {
             const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
             const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
             Window Aw = e->source(a, z, first, mid, first, mid);
@@ -631,7 +817,7 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
                               void* stream) {
   BI_REQUIRE(e != nullptr, "null engine");
   BI_REQUIRE(m && minv && workspace, "null buffer");
-  BI_REQUIRE(ldm >= e->n && ldi >= e->n, "leading dimension smaller than the matrix order");
+  BI_REQUIRE(ldm >= e->w && ldi >= e->w, "leading dimension smaller than the owned columns");
   BI_REQUIRE(workspace_bytes >= bi_engine_workspace_bytes(e), "workspace too small");
   for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
   e->graphs.clear();
@@ -652,6 +838,15 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   }
   e->info = reinterpret_cast<int*>(p);
   p += align256(e->info_ints * 4);
+  e->X = reinterpret_cast<double*>(p);
+  p += align256(e->x_elems * 8);
+  e->sendbuf = reinterpret_cast<double*>(p);
+  p += align256(e->send_elems * 8);
+  e->recvbuf = reinterpret_cast<double*>(p);
+  p += align256(e->recv_elems * 8);
+  cudaGetDevice(&e->device);
+  for (auto& kv : e->seg_graphs) cudaGraphExecDestroy(kv.second);
+  e->seg_graphs.clear();
   BI_CUDA_TRY(init_attributes());
   {
     // BI_PRIORITY_MODE: 0 none; 1 lane order (lane 0 highest); 2 leaf kernels
@@ -798,6 +993,14 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
   BI_CUDA_TRY(cudaMemcpyAsync(meta, host_meta.data(), host_meta.size(), cudaMemcpyHostToDevice,
                               static_cast<cudaStream_t>(stream)));
   BI_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  // flat op list of the (single) lane: the shard segment driver walks it
+  e->flat.clear();
+  e->step_first_op.assign(e->nsteps + 2, 0);
+  for (int st = 1; st <= e->nsteps; ++st) {
+    e->step_first_op[st] = (int)e->flat.size();
+    for (const Op& op : e->lane_ops[0][st]) e->flat.push_back({st, op});
+  }
+  e->step_first_op[e->nsteps + 1] = (int)e->flat.size();
   e->bound = true;
   return 0;
 }
@@ -830,6 +1033,7 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
         }
     }
     for (const Op& op : step_ops) {
+      if (op.kind == 3) continue;  // exchanges: shard driver only (P > 1)
       if (!(mask & (op.kind == 0 ? 2 : 1))) continue;
       cudaError_t err;
       if (split_io && stepid == e->nsteps && &op == &step_ops.back() && op.kind == 1) {
@@ -1116,6 +1320,7 @@ static int run_impl(bi_engine* e, int first_step, int last_step, int use_graph, 
 
 extern "C" int bi_engine_run(bi_engine* e, int first_step, int last_step, int use_graph, void* stream) {
   BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(e->P == 1, "a column-sharded engine runs through bi_engine_run_ops / bi_shard_group_run");
   BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step,
              "stepid outside 1..N_s");
   return run_impl(e, first_step, last_step, use_graph, static_cast<cudaStream_t>(stream), nullptr);
@@ -1314,6 +1519,7 @@ extern "C" int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t l
                                   double* host_out, int64_t ld_out, int64_t stride_out, int first_step,
                                   int last_step, int use_graph, void* stream) {
   BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(e->P == 1, "a column-sharded engine runs through bi_engine_run_ops / bi_shard_group_run");
   BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step,
              "stepid outside 1..N_s");
   BI_REQUIRE(!host_in || (ld_in >= e->n && (e->Z == 1 || stride_in >= ld_in * e->n)),
@@ -1336,6 +1542,7 @@ extern "C" int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t l
 
 extern "C" int bi_engine_run_phase(bi_engine* e, int first_step, int last_step, int mask, void* stream) {
   BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(e->P == 1, "a column-sharded engine runs through bi_engine_run_ops / bi_shard_group_run");
   BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step, "stepid outside 1..N_s");
   BI_REQUIRE(mask >= 1 && mask <= 3, "mask must be 1 (GEMM ops), 2 (leaf inversions) or 3");
   e->last_stream = static_cast<cudaStream_t>(stream);
@@ -1371,7 +1578,7 @@ extern "C" int bi_engine_launches(const bi_engine* e, int first_step, int last_s
   for (int lane = 0; lane < e->nlanes; ++lane)
   for (int stepid = first_step; stepid <= last_step; ++stepid)
     for (const Op& op : e->lane_ops[lane][stepid]) {
-      if (op.kind == 2) continue;  // copy, not a kernel
+      if (op.kind == 2 || op.kind == 3) continue;  // copy / exchange, not a kernel
       if (op.kind == 1) {
         gemm += 1;
       } else {
@@ -1504,5 +1711,253 @@ extern "C" int bi_engine_tset_square(const bi_engine* e, int level, int quad, in
 
 extern "C" int bi_engine_destroy(bi_engine* e) {
   delete e;
+  return 0;
+}
+
+// ===========================================================================
+// Column-sharded ranks: segments of local ops between exchanges
+// ===========================================================================
+
+extern "C" int bi_engine_shard_segments(const bi_engine* e, int first_step, int last_step, int* begin, int* end,
+                                        int* xchg, int cap) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(first_step >= 1 && last_step <= e->nsteps && first_step <= last_step, "stepid outside 1..N_s");
+  int n = 0, b = e->step_first_op[first_step];
+  const int stop = e->step_first_op[last_step + 1];
+  for (int i = b; i <= stop; ++i) {
+    const bool at_x = i < stop && e->flat[i].op.kind == 3;
+    if (i == stop || at_x) {
+      if (n < cap) {
+        begin[n] = b;
+        end[n] = i;
+        xchg[n] = at_x ? e->flat[i].op.index : -1;
+      }
+      ++n;
+      b = i + 1;
+    }
+  }
+  return n;
+}
+
+static cudaError_t enqueue_flat(bi_engine* e, int b, int en, cudaStream_t s) {
+  for (int i = b; i < en; ++i) {
+    const Op& op = e->flat[i].op;
+    cudaError_t err = cudaSuccess;
+    if (op.kind == 0) {
+      PriorityScope leaf_prio(e->leaf_priority ? e->leaf_priority : g_launch_priority);
+      err = launch_inv_group(e->invs[op.index].g, s);
+    } else if (op.kind == 1) {
+      GemmCapScope cap(e->gemm_cap);
+      const GemmLaunchRec& L = e->launches[op.index];
+      err = launch_gemm(e->descs.data() + L.first, e->d_descs + L.first, L.count, s);
+    }
+    if (err != cudaSuccess) return err;
+  }
+  return cudaSuccess;
+}
+
+static int run_ops_impl(bi_engine* e, int b, int en, int use_graph, cudaStream_t s) {
+  e->last_stream = s;
+  if (b >= en) return 0;
+  e->set_policy(0);
+  if (!use_graph) {
+    BI_CUDA_TRY(enqueue_flat(e, b, en, s));
+    return 0;
+  }
+  auto key = std::make_pair(b, en);
+  auto it = e->seg_graphs.find(key);
+  if (it == e->seg_graphs.end()) {
+    if (!e->capture_stream) BI_CUDA_TRY(cudaStreamCreateWithFlags(&e->capture_stream, cudaStreamNonBlocking));
+    BI_CUDA_TRY(cudaStreamBeginCapture(e->capture_stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t err = enqueue_flat(e, b, en, e->capture_stream);
+    cudaGraph_t graph = nullptr;
+    cudaError_t err2 = cudaStreamEndCapture(e->capture_stream, &graph);
+    if (err != cudaSuccess || err2 != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      set_error(std::string("segment capture failed: ") + cudaGetErrorString(err != cudaSuccess ? err : err2));
+      return 3;
+    }
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t err3 = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+    cudaGraphDestroy(graph);
+    BI_CUDA_TRY(err3);
+    it = e->seg_graphs.emplace(key, exec).first;
+  }
+  BI_CUDA_TRY(cudaGraphLaunch(it->second, s));
+  return 0;
+}
+
+extern "C" int bi_engine_run_ops(bi_engine* e, int op_begin, int op_end, int use_graph, void* stream) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(op_begin >= 0 && op_begin <= op_end && op_end <= (int)e->flat.size(), "op range out of bounds");
+  for (int i = op_begin; i < op_end; ++i) BI_REQUIRE(e->flat[i].op.kind != 3, "op range spans an exchange");
+  // the executed step range, for bi_engine_status (a run starts at op 0)
+  if (op_begin == 0) {
+    e->last_first = 1;
+    e->last_last = 0;
+  }
+  if (op_end > op_begin) e->last_last = std::max(e->last_last, e->flat[op_end - 1].stepid);
+  return run_ops_impl(e, op_begin, op_end, use_graph, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int bi_engine_shard_info(const bi_engine* e, int64_t out[8]) {
+  BI_REQUIRE(e && out, "null argument");
+  out[0] = e->P;
+  out[1] = e->rank;
+  out[2] = e->col0;
+  out[3] = e->w;
+  out[4] = e->wmax;
+  out[5] = (int64_t)e->xchgs.size();
+  out[6] = e->send_elems;
+  out[7] = e->recv_elems;
+  return 0;
+}
+
+extern "C" int bi_engine_xchg_desc(const bi_engine* e, int i, int64_t out[8]) {
+  BI_REQUIRE(e && e->bound && out, "engine not bound");
+  BI_REQUIRE(i >= 0 && i < (int)e->xchgs.size(), "exchange index out of range");
+  const auto& x = e->xchgs[i];
+  out[0] = x.g0;
+  out[1] = x.gs;
+  out[2] = x.rows;
+  out[3] = e->wmax;
+  out[4] = x.in_a;
+  out[5] = x.from0;
+  out[6] = x.from1;
+  out[7] = x.kind * 100 + x.level;
+  return 0;
+}
+
+extern "C" int bi_engine_shard_buffers(const bi_engine* e, double** sendbuf, double** recvbuf) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  if (sendbuf) *sendbuf = e->sendbuf;
+  if (recvbuf) *recvbuf = e->recvbuf;
+  return 0;
+}
+
+// this rank's send parts -> the contiguous send area (rows x wmax, for an all-gather)
+extern "C" int bi_engine_xchg_pack(bi_engine* e, int i, void* stream) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(i >= 0 && i < (int)e->xchgs.size(), "exchange index out of range");
+  BI_REQUIRE(e->send_elems > 0, "engine created without BI_SHARD_STAGING");
+  const auto& x = e->xchgs[i];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  BI_CUDA_TRY(cudaMemcpy2DAsync(e->sendbuf, e->wmax * 8, x.top, x.top_ld * 8, e->w * 8, x.top_rows,
+                                cudaMemcpyDeviceToDevice, s));
+  if (x.bot)
+    BI_CUDA_TRY(cudaMemcpy2DAsync(e->sendbuf + x.top_rows * e->wmax, e->wmax * 8, x.bot, x.bot_ld * 8, e->w * 8,
+                                  x.bot_rows, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+// the group's gathered send areas ([gs][rows][wmax]) -> X (the needed members' columns side by side)
+extern "C" int bi_engine_xchg_unpack(bi_engine* e, int i, void* stream) {
+  BI_REQUIRE(e && e->bound, "engine not bound");
+  BI_REQUIRE(i >= 0 && i < (int)e->xchgs.size(), "exchange index out of range");
+  BI_REQUIRE(e->recv_elems > 0, "engine created without BI_SHARD_STAGING");
+  const auto& x = e->xchgs[i];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int m = x.from0; m < x.from1; ++m) {
+    const int64_t c0 = e->off[(size_t)m * e->nbp], wm = e->off[(size_t)(m + 1) * e->nbp] - c0;
+    BI_CUDA_TRY(cudaMemcpy2DAsync(e->X + (c0 - x.x_col0), x.ldx * 8, e->recvbuf + (int64_t)(m - x.g0) * x.rows * e->wmax,
+                                  e->wmax * 8, wm * 8, x.rows, cudaMemcpyDeviceToDevice, s));
+  }
+  return 0;
+}
+
+// All P ranks in this process (one engine per GPU, or several on one GPU for
+// tests): one host thread enqueues every rank's segments in order; each
+// exchange is peer copies of the members' send windows straight into the
+// reader's X on the reader's stream, ordered by events (no host barrier, no
+// staging); a rank's next segment waits until its group has copied.
+extern "C" int bi_shard_group_run(bi_engine** es, int P, void* const* streams, int first_step, int last_step,
+                                  int use_graph) {
+  BI_REQUIRE(es && streams && P >= 1, "null argument");
+  for (int r = 0; r < P; ++r) {
+    BI_REQUIRE(es[r] && es[r]->bound && es[r]->P == P && es[r]->rank == r, "engines must be ranks 0..P-1 of one run");
+    BI_REQUIRE(first_step >= 1 && last_step <= es[r]->nsteps && first_step <= last_step, "stepid outside 1..N_s");
+  }
+  int cur = 0;
+  BI_CUDA_TRY(cudaGetDevice(&cur));
+  std::vector<std::vector<int>> B(P), E(P), Xi(P);
+  int nseg = -1;
+  for (int r = 0; r < P; ++r) {
+    const int n = bi_engine_shard_segments(es[r], first_step, last_step, nullptr, nullptr, nullptr, 0);
+    B[r].resize(n);
+    E[r].resize(n);
+    Xi[r].resize(n);
+    bi_engine_shard_segments(es[r], first_step, last_step, B[r].data(), E[r].data(), Xi[r].data(), n);
+    BI_REQUIRE(nseg < 0 || n == nseg, "ranks disagree on the exchange schedule");
+    nseg = n;
+  }
+  std::vector<cudaEvent_t> done(P), copied(P);
+  auto cleanup = [&]() {
+    for (int r = 0; r < P; ++r) {
+      cudaSetDevice(es[r]->device);
+      if (done[r]) cudaEventDestroy(done[r]);
+      if (copied[r]) cudaEventDestroy(copied[r]);
+    }
+    cudaSetDevice(cur);
+  };
+  auto fail = [&](cudaError_t err) {
+    cleanup();
+    set_error(std::string("bi_shard_group_run: ") + cudaGetErrorString(err));
+    return 3;
+  };
+  for (int r = 0; r < P; ++r) {
+    es[r]->last_first = first_step;  // for bi_engine_status
+    es[r]->last_last = last_step;
+    cudaSetDevice(es[r]->device);
+    cudaError_t err = cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming);
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&copied[r], cudaEventDisableTiming);
+    if (err == cudaSuccess && first_step == 1)
+      err = cudaMemset2DAsync(es[r]->Minv, es[r]->ldi * 8, 0, es[r]->w * 8, es[r]->n,
+                              static_cast<cudaStream_t>(streams[r]));
+    if (err != cudaSuccess) return fail(err);
+  }
+  for (int k = 0; k < nseg; ++k) {
+    for (int r = 0; r < P; ++r) {
+      bi_engine* e = es[r];
+      cudaStream_t s = static_cast<cudaStream_t>(streams[r]);
+      cudaSetDevice(e->device);
+      if (k > 0 && Xi[r][k - 1] >= 0) {  // my send windows are free once my group copied them
+        const auto& px = e->xchgs[Xi[r][k - 1]];
+        for (int m = px.g0; m < px.g0 + px.gs; ++m) {
+          cudaError_t err = cudaStreamWaitEvent(s, copied[m], 0);
+          if (err != cudaSuccess) return fail(err);
+        }
+      }
+      int rc = run_ops_impl(e, B[r][k], E[r][k], use_graph, s);
+      if (rc) {
+        cleanup();
+        return rc;
+      }
+      cudaError_t err = cudaEventRecord(done[r], s);
+      if (err != cudaSuccess) return fail(err);
+    }
+    for (int r = 0; r < P; ++r) {
+      if (Xi[r][k] < 0) continue;
+      bi_engine* e = es[r];
+      cudaStream_t s = static_cast<cudaStream_t>(streams[r]);
+      cudaSetDevice(e->device);
+      const auto& x = e->xchgs[Xi[r][k]];
+      for (int m = x.from0; m < x.from1; ++m) {
+        const auto& mx = es[m]->xchgs[Xi[m][k]];
+        cudaError_t err = cudaStreamWaitEvent(s, done[m], 0);
+        const int64_t c0 = es[m]->col0 - x.x_col0;
+        if (err == cudaSuccess)
+          err = cudaMemcpy2DAsync(e->X + c0, x.ldx * 8, mx.top, mx.top_ld * 8, es[m]->w * 8, mx.top_rows,
+                                  cudaMemcpyDefault, s);
+        if (err == cudaSuccess && mx.bot)
+          err = cudaMemcpy2DAsync(e->X + mx.top_rows * x.ldx + c0, x.ldx * 8, mx.bot, mx.bot_ld * 8, es[m]->w * 8,
+                                  mx.bot_rows, cudaMemcpyDefault, s);
+        if (err != cudaSuccess) return fail(err);
+      }
+      cudaError_t err = cudaEventRecord(copied[r], s);
+      if (err != cudaSuccess) return fail(err);
+    }
+  }
+  // events may be destroyed while pending work still references them (CUDA defers the release)
+  cleanup();
   return 0;
 }

@@ -537,18 +537,93 @@ class ShardedEngine:
         return out
 
 
+class NativeShardDist:
+    """This process's rank of the native column-sharded engine (shard.py),
+    exchanging over a torch.distributed group (NCCL)."""
+
+    def __init__(self, sizes, group=None, dist=None):
+        if dist is None:
+            import torch.distributed as dist
+        from .shard import NativeShard, make_groups
+
+        self.dist = dist
+        self.group = group if group is not None else dist.group.WORLD
+        P, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        self.shard = NativeShard(sizes, P, rank, staging=True)
+        self.groups = make_groups(dist, P, self.group)
+        self.P, self.rank, self.n = P, rank, self.shard.n
+        self._last = self.shard.n_steps
+
+    def load(self, m) -> None:
+        self.shard.load(m)
+
+    def run(self, first: int = 1, last: int | None = None) -> None:
+        nsteps = self.shard.n_steps
+        last = nsteps if last is None else max(first, min(int(last), nsteps))
+        self._last = last
+        self.shard.run_dist(self.dist, self.groups, first, last)
+
+    def check(self) -> None:
+        """SingularBlock(step, quad) of the earliest singular leaf on any rank (collective)."""
+        import torch
+
+        fail = self.shard.check()
+        nb = len(self.shard.sizes)
+        mine = fail or (1 << 30, 1 << 30)
+        t = torch.tensor([mine[0] * (nb + 1) + mine[1]], dtype=torch.int64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.to(self.shard.M.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        v = int(t.item())
+        if v < (1 << 30) * (nb + 1):
+            raise SingularBlock("A", path=[], step=v // (nb + 1), quad=v % (nb + 1))
+
+    def launches(self) -> int:
+        return self.shard.launches(1, self._last)
+
+    def gather(self, root: int = 0):
+        """The full inverse on ``root`` (None elsewhere): slabs sent one at a time."""
+        import torch
+
+        sh = self.shard
+        glob = (lambda r: r) if self.group is self.dist.group.WORLD else \
+            (lambda r: self.dist.get_global_rank(self.group, r))
+        nccl = self.dist.get_backend(self.group) == "nccl"
+        buf = torch.zeros((sh.n, sh.wmax), dtype=torch.float64, device=sh.M.device if nccl else "cpu")
+        out = np.empty((sh.n, sh.n)) if self.rank == root else None
+        off = sh.scheme.offsets
+        nbp = len(sh.sizes) // self.P
+        for r in range(self.P):
+            if r == root:
+                if self.rank == root:
+                    sh.write_slab(out)
+                continue
+            c0, c1 = off[r * nbp], off[(r + 1) * nbp]
+            if self.rank == r:
+                buf[:, :sh.w] = sh.Minv[0]
+                self.dist.send(buf, dst=glob(root), group=self.group)
+            elif self.rank == root:
+                self.dist.recv(buf, src=glob(r), group=self.group)
+                out[:, c0:c1] = buf[:, :c1 - c0].cpu().numpy()
+        return out
+
+
 def sharded_engine(sizes, group=None):
-    """This process's rank of the column-sharded engine (one process per GPU,
-    torch.distributed NCCL group)."""
-    return ShardedEngine(sizes, group=group)
+    """This process's rank of the column-sharded engine (one process per
+    GPU, torch.distributed NCCL group): the native engine."""
+    return NativeShardDist(sizes, group=group)
 
 
 def run_inversion_sharded(m, sizes, group=None, backend=None, stop_after_step=None, dist=None, root: int = 0):
     """run_inversion (engine.py:482-542) with the matrix column-sharded over the
     ranks of ``group`` (one process per GPU).  Every rank passes the same
     ``m``; rank ``root`` receives the full inverse, the others None.  Raises
-    SingularBlock like the single-device engine."""
-    eng = ShardedEngine(sizes, group=group, backend=backend, dist=dist)
+    SingularBlock like the single-device engine.  The native engine runs
+    unless a compute ``backend`` is given (CPU tests of the schedule)."""
+    if backend is None:
+        eng = NativeShardDist(sizes, group=group, dist=dist)
+    else:
+        eng = ShardedEngine(sizes, group=group, backend=backend, dist=dist)
     eng.load(np.asarray(m, dtype=np.float64))
     eng.run(1, stop_after_step)
     eng.check()
@@ -556,18 +631,25 @@ def run_inversion_sharded(m, sizes, group=None, backend=None, stop_after_step=No
 
 
 def run_inversion_local(m, sizes, gpus: int, stop_after_step=None, devices=None, backend_factory=None) -> np.ndarray:
-    """The sharded schedule on ``gpus`` GPUs of THIS process (one thread per
-    GPU, slabs exchanged by peer copies; local_group.py).  ``devices``
-    overrides the thread -> device map (tests run several "GPUs" on one);
-    ``backend_factory`` replaces the device backend (CPU tests)."""
+    """The sharded schedule on ``gpus`` GPUs of THIS process.  Default: the
+    native engine, all ranks driven by one native call with peer-copy
+    exchanges (shard.run_inversion_group).  ``backend_factory`` (CPU tests)
+    or BI_FUSED_GATHER=1 (K1P, DESIGN 7) run the host-driven ShardedEngine on
+    one thread per GPU (local_group.py).  ``devices`` overrides the rank ->
+    device map (tests run several ranks on one GPU)."""
+    import os
+
     from .local_group import run_threads
 
     m = np.asarray(m, dtype=np.float64)
+    if backend_factory is None and os.environ.get("BI_FUSED_GATHER", "0") != "1":
+        from .shard import run_inversion_group
+
+        return run_inversion_group(m, sizes, gpus, stop_after_step=stop_after_step, devices=devices)
     if backend_factory is None:  # peer access between the participating devices (bi_init)
         from . import _lib
 
         _lib.init_devices(sorted(set(devices if devices is not None else range(gpus))))
-
     out = np.empty(m.shape)
 
     def target(dist, rank):

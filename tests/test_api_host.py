@@ -126,9 +126,14 @@ def test_reference_signature_checkpoint_roundtrip(tmp_path):
     files = _golden_ckpt_files()
     written = {str(p.relative_to(dst)): p.read_bytes() for p in dst.rglob("*") if p.is_file()}
     assert written == files
-    store, fresh = storage.fresh_state(dst, scheme, file_backed=True)  # drops stale state
-    assert not (dst / "meta.json").exists() and not list(dst.rglob("*.blk"))
-    assert np.count_nonzero(store.data) == 0 and set(fresh) == {1, 2}
+    store, fresh = storage.fresh_state(dst, scheme, file_backed=True)  # drops stale state (storage.py:391-411)
+    assert not (dst / "meta.json").exists() and not list((dst / "tset").rglob("*.blk"))
+    assert isinstance(store, storage.FileBlockStore)  # zeroed M_inv block files, as the reference writes them
+    assert sorted(p.name for p in (dst / "minv").glob("*.blk")) == sorted(f"B_{i}_{j}.blk" for i in range(4)
+                                                                          for j in range(4))
+    assert np.count_nonzero(store.to_dense()) == 0 and set(fresh) == {1, 2}
+    mem, _ = storage.fresh_state(dst, scheme, file_backed=False)
+    assert np.count_nonzero(mem.data) == 0
 
 
 def test_cli_parser_and_host_commands(tmp_path, capsys):
