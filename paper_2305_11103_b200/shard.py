@@ -59,7 +59,6 @@ class NativeShard:
         info = (_lib._c_i64 * 8)()
         _lib.check(L.bi_engine_shard_info(h, info), "bi_engine_shard_info")
         self.c0, self.w, self.wmax = int(info[2]), int(info[3]), int(info[4])
-        self.n_xchg = int(info[5])
         self.M = _lib.empty_matrix(self.n, self.w, batch=1)
         self.Minv = _lib.empty_matrix(self.n, self.w, batch=1)
         self.ws = _lib.workspace(L.bi_engine_workspace_bytes(h))
@@ -67,6 +66,8 @@ class NativeShard:
             _lib.check(L.bi_engine_bind(h, _lib.ptr(self.M), _lib.ld(self.M), int(self.M.stride(0)),
                                         _lib.ptr(self.Minv), _lib.ld(self.Minv), int(self.Minv.stride(0)),
                                         _lib.ptr(self.ws), self.ws.numel(), _lib.stream_ptr()), "bi_engine_bind")
+        _lib.check(L.bi_engine_shard_info(h, info), "bi_engine_shard_info")  # exchanges exist once bound
+        self.n_xchg = int(info[5])
         self._segs = {}
         self._x = [self.xchg_desc(i) for i in range(self.n_xchg)]
         if staging:
