@@ -50,6 +50,19 @@
 namespace bi {
 namespace {
 
+// Ring-stage release by the consumer warps (lane 0 after __syncwarp, which
+// orders the warp's shared-memory reads of the stage before it): a
+// release/acquire pair around the counter, so every warp's generic-proxy
+// reads of the stage happen-before the last warp's async-proxy (TMA) refill
+// of it (fence.proxy.async follows in fill()).  Returns true for the last warp.
+__device__ __forceinline__ bool release_stage(unsigned* counter, unsigned warps) {
+  __threadfence_block();  // release: this warp's reads of the stage
+  if (atomicAdd(counter, 1u) != warps - 1) return false;
+  __threadfence_block();  // acquire: every other warp's reads
+  return true;
+}
+
+
 constexpr int kWarps = kK1Warps;
 constexpr int kThreads = kK1Threads;
 constexpr int kBoxBBytes = kK1BoxB;
@@ -243,7 +256,7 @@ __global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks
       mbar_wait(&full[stage], (cons_it / kStages) & 1);
       k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
       __syncwarp();
-      if (lane == 0 && atomicAdd(&released[stage], 1u) == Cfg::kWarpsT - 1) {
+      if (lane == 0 && release_stage(&released[stage], Cfg::kWarpsT)) {
         released[stage] = 0;
         fill(stage, tile, tc, KT, kt + kStages);
       }
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks
       mbar_wait(&full[stage], (cons_it / kStages) & 1);
       k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
       __syncwarp();
-      if (lane == 0 && atomicAdd(&released[stage], 1u) == Cfg::kWarpsT - 1) {
+      if (lane == 0 && release_stage(&released[stage], Cfg::kWarpsT)) {
         released[stage] = 0;
         fill(stage, tile, kt + kStages);
       }
@@ -472,7 +485,7 @@ __global__ void __launch_bounds__(RefillCfg<64>::kThr, RefillCfg<64>::kMinBlocks
       }
       k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
       __syncwarp();
-      if (lane == 0 && atomicAdd(&released[stage], 1u) == Cfg::kWarpsT - 1) {
+      if (lane == 0 && release_stage(&released[stage], Cfg::kWarpsT)) {
         released[stage] = 0;
         if (cons_it + kStages < iters) {  // a refill follows (same test in every CTA)
           mbar_arrive_remote(&empty[stage], 0);
