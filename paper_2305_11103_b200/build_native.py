@@ -37,14 +37,19 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, extra: list | None = None) -> Path:
+    """Compile and link; ``out``/``extra`` build a variant (e.g. -DBI_K1_GROUP_M=8)
+    elsewhere for A/B timing through BI_LIB, leaving the in-tree library alone."""
+    if out is None and not force and not needs_build():
         return LIB
-    OBJDIR.mkdir(parents=True, exist_ok=True)
+    target = LIB if out is None else Path(out)
+    objdir = OBJDIR if out is None else target.parent / (target.stem + "_obj")
+    objdir.mkdir(parents=True, exist_ok=True)
+    extra = list(extra or [])
 
     def compile_one(src: str) -> Path:
-        obj = OBJDIR / (Path(src).stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
+        obj = objdir / (Path(src).stem + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -54,13 +59,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
         objs = list(pool.map(compile_one, SOURCES))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = target.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

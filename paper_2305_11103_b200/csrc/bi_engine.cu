@@ -670,9 +670,22 @@ static int build_schedule(bi_engine* e) {
     } else {
       const int lv = a.sid;
       std::vector<GemmDesc> l1, l2;
+      // Quad order: sources in T_cid put 2^(cid-sid) level-sid quads on the
+      // diagonal of each T_cid square -- a uniform stride inside a square, a
+      // jump between squares.  Visiting the quads as (position in square,
+      // square) when there are fewer positions than squares makes every
+      // position class one strided batch, so a launch carries at most 4
+      // descriptors per product and stays on the TMA path (ncu r02: 88
+      // launches had fallen back to the cp.async descriptor-table kernel).
+      const int qlo = e->h0 >> lv, qn = (e->h1 >> lv) - qlo;
+      const int per_sq = (a.from_tset && !e->is_global(a.cid)) ? std::min(qn, 1 << (a.cid - lv)) : 1;
+      const int nsq = qn / per_sq;
+      const bool by_pos = per_sq > 1 && per_sq <= nsq;
+      auto quad_at = [&](int i) { return qlo + (by_pos ? (i % nsq) * per_sq + i / nsq : i); };
       for (int kind = 0; kind < 2; ++kind)
         for (int z = Z0; z < Z1; ++z)
-          for (int g = (e->h0 >> lv); g < (e->h1 >> lv); ++g) {
+          for (int gi = 0; gi < qn; ++gi) {
+            const int g = quad_at(gi);
             const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
             const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
             Window B = e->source(a, z, first, mid, mid, last);
@@ -687,7 +700,8 @@ static int build_schedule(bi_engine* e) {
           }
       for (int kind = 0; kind < 2; ++kind)
         for (int z = Z0; z < Z1; ++z)
-          for (int g = (e->h0 >> lv); g < (e->h1 >> lv); ++g) {
+          for (int gi = 0; gi < qn; ++gi) {
+            const int g = quad_at(gi);
             const int first = g << lv, mid = first + (1 << (lv - 1)), last = (g + 1) << lv;
             const int64_t ha = off[mid] - off[first], hd = off[last] - off[mid];
             Window Aw = e->source(a, z, first, mid, first, mid);

@@ -71,10 +71,13 @@ constexpr int kStageBytes = kK1Stage;
 template <int S>
 constexpr int smem_bytes() { return S * kStageBytes + 1024; }  // + alignment slack
 
+// Up to kTmaInline descriptors ride in the kernel parameters (2 tensor maps +
+// the descriptor each: ~3.2 KB for 8; sm_100 allows 32 KB of parameters).
+constexpr int kTmaInline = 8;
 struct alignas(64) TmaLaunch {
-  CUtensorMap ta[kGemmInline];
-  CUtensorMap tb[kGemmInline];
-  GemmDesc d[kGemmInline];
+  CUtensorMap ta[kTmaInline];
+  CUtensorMap tb[kTmaInline];
+  GemmDesc d[kTmaInline];
   int count, total_tiles;
 };
 
@@ -612,7 +615,7 @@ bool launch_gemm_kseg_tma(const GemmDesc& d, int nseg, const double* const* a, c
 // descriptors do not qualify (caller falls back to the cp.async kernel).
 bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t stream, cudaError_t* err) {
   *err = cudaSuccess;
-  if (count <= 0 || count > kGemmInline) return false;
+  if (count <= 0 || count > kTmaInline) return false;
   if (tma_init() != cudaSuccess) return false;
   TmaLaunch L;
   std::memset(&L, 0, sizeof(L));
