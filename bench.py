@@ -328,6 +328,20 @@ def _secondary_cfg2(bi, steps: int, warmup: int) -> dict:
         out[sched] = {"ms_per_batch": t, "value": CFG2_BATCH * nominal_flops(CFG2_N) / (t * 1e-3) / 1e12,
                       "unit": UNIT, "residual_fro_max": float(np.max(fro))}
         del eng
+    bi.release_engines()
+    # one cfg2 matrix through the reference-signature call on a NumPy array (e2e)
+    import torch
+
+    e2e = []
+    for i in range(3 + steps):
+        a, b = _events()
+        a.record()
+        bi.run_inversion(ms[0], sizes=sizes)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            e2e.append(a.elapsed_time(b))
+    out["one_matrix_e2e_ms"] = sum(e2e) / len(e2e)
     return out
 
 

@@ -1025,6 +1025,18 @@ static cudaError_t copy_top_quads(bi_engine* e, int lane, const HostIO* io, bool
 static cudaError_t pass_in_chunks(bi_engine* e, int lane, const GemmLaunchRec& L, const HostIO* io,
                                   cudaStream_t s);
 
+// BI_LEAF_GEMM_CAP: SMs the leaf chain's own trailing-update GEMMs may use
+// (persistent grid of 2 CTAs per SM); 0 = uncapped.  A narrow grid starts
+// as soon as a few SMs free up instead of waiting for a GPU's worth of
+// another lane's GEMM tiles to retire.
+static int leaf_gemm_cap() {
+  static const int cap = [] {
+    const char* v = getenv("BI_LEAF_GEMM_CAP");
+    return v ? atoi(v) : 0;
+  }();
+  return cap;
+}
+
 static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cudaStream_t s, int mask,
                                 cudaEvent_t after_first = nullptr, bool wait_input = false,
                                 const HostIO* split_io = nullptr) {
@@ -1070,6 +1082,7 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
         }();
         if (skip_leaves) continue;
         PriorityScope leaf_prio(e->leaf_priority ? e->leaf_priority : g_launch_priority);
+        GemmCapScope leaf_cap(leaf_gemm_cap());
         err = launch_inv_group(e->invs[op.index].g, s);
       } else if (split_io && stepid == e->nsteps && &op == &step_ops.back() &&
                  e->launches[op.index].count <= kGemmInline) {

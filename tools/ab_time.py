@@ -28,7 +28,7 @@ def t(eng, reps):
 
 out = {"lib": os.environ.get("BI_LIB", "in-tree")}
 m, sizes = cfg4()
-for sched in ("eq7", "pivot_a"):
+for sched in (() if "--cfg2-only" in sys.argv else ("eq7", "pivot_a")):
     e = bi.DeviceEngine(sizes, schedule=sched)
     e.load(m)
     out[f"cfg4_{sched}_ms"] = t(e, 5)
