@@ -21,12 +21,16 @@
 //    to (step, quad, matrix) after the range (no host syncs inside it).
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
 #include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <string>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <tuple>
 #include <vector>
@@ -1376,12 +1380,77 @@ struct Region {
   int64_t rows, bytes;
 };
 
+// Persistent host worker threads for the staging copies (spawning a thread
+// per piece cost ~1-2 ms per call at cfg2 size).  run(T, f) runs f(0..T-1),
+// f(0) on the caller, and returns when all are done.  One run at a time.
+class CopyPool {
+ public:
+  void run(int T, const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> one(run_mu_);
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      while ((int)threads_.size() < T - 1) {
+        const int id = (int)threads_.size();
+        threads_.emplace_back([this, id] { loop(id); });
+      }
+      job_ = &f;
+      active_ = T - 1;
+      pending_ = T - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+
+ private:
+  void loop(int id) {
+    int seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job = nullptr;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        if (id >= active_) continue;
+        job = job_;
+      }
+      (*job)(id + 1);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> threads_;
+  const std::function<void(int)>* job_ = nullptr;
+  int active_ = 0, pending_ = 0, gen_ = 0;
+  bool stop_ = false;
+};
+
+static void copy_pool_run(int T, const std::function<void(int)>& f) {
+  static CopyPool* pool = new CopyPool();  // process lifetime (never joined at exit)
+  pool->run(T, f);
+}
+
 // dst/src 2-D regions copied by up to `threads` host threads, split by rows
 static void par_copy(const std::vector<Region>& regs, int threads) {
   int64_t total = 0;
   for (const Region& r : regs) total += r.rows * r.bytes;
   if (total == 0) return;
-  const int64_t per = 4 << 20;
+  const int64_t per = 1 << 20;  // >= 1 MB per thread
   int T = (int)std::max<int64_t>(1, std::min<int64_t>(threads, total / per));
   if (T == 1) {
     for (const Region& r : regs)
@@ -1407,10 +1476,7 @@ static void par_copy(const std::vector<Region>& regs, int threads) {
       pos += sz;
     }
   };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
-  work(0);
-  for (auto& th : pool) th.join();
+  copy_pool_run(T, work);
 }
 
 static int host_threads() {
@@ -1483,28 +1549,46 @@ static int run_host_pipelined(bi_engine* e, const double* in, int64_t ld_in, int
   HostIO io{nullptr, 0, 0, nullptr, 0, 0};
   std::vector<std::array<int, 4>> blocks;
   int done = 0;  // last step enqueued
+  static const bool trace = getenv("BI_PIPE_TRACE") != nullptr;
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t_start = trace ? now_us() : 0.0;
   for (int lv = 0; lv <= e->k; ++lv) {
+    const double t_lv = trace ? now_us() : 0.0;
     if (in) {
       level_blocks(e, lv, blocks);
-      if (!in_pinned) {  // host: user rows -> staging, same coordinates
-        std::vector<Region> regs;
-        for (int z = 0; z < e->Z; ++z)
-          for (const auto& b : blocks) {
+      // the level's (matrix, block) pieces in up to 4 chunks: the DMA of a
+      // chunk runs while the host stages the next one
+      std::vector<std::pair<int, std::array<int, 4>>> pieces;
+      for (int z = 0; z < e->Z; ++z)
+        for (const auto& b : blocks) pieces.push_back({z, b});
+      const int nch = std::min<int>(4, (int)pieces.size());
+      for (int c = 0; c < nch; ++c) {
+        const size_t p0 = pieces.size() * c / nch, p1 = pieces.size() * (c + 1) / nch;
+        if (!in_pinned) {  // host: user rows -> staging, same coordinates
+          std::vector<Region> regs;
+          for (size_t i = p0; i < p1; ++i) {
+            const int z = pieces[i].first;
+            const auto& b = pieces[i].second;
             const int64_t ro = e->off[b[0]], co = e->off[b[2]];
             regs.push_back({(char*)(e->stage_in + (int64_t)z * src_s + ro * src_ld + co),
                             (const char*)(in + (int64_t)z * s_in + ro * ld_in + co), src_ld * 8, ld_in * 8,
                             e->off[b[1]] - ro, (e->off[b[3]] - co) * 8});
           }
-        par_copy(regs, T);
-      }
-      for (int z = 0; z < e->Z; ++z)
-        for (const auto& b : blocks) {
+          par_copy(regs, T);
+        }
+        for (size_t i = p0; i < p1; ++i) {
+          const int z = pieces[i].first;
+          const auto& b = pieces[i].second;
           const int64_t ro = e->off[b[0]], co = e->off[b[2]];
           BI_CUDA_TRY(cudaMemcpy2DAsync(const_cast<double*>(e->M) + (int64_t)z * e->sm + ro * e->ldm + co,
                                         e->ldm * 8, src + (int64_t)z * src_s + ro * src_ld + co, src_ld * 8,
                                         (e->off[b[3]] - co) * 8, e->off[b[1]] - ro, cudaMemcpyHostToDevice,
                                         e->copy_stream));
         }
+      }
+      if (trace) fprintf(stderr, "[pipe] level %d host copy %.0f us (t=%.0f)\n", lv, now_us() - t_lv, now_us() - t_start);
       BI_CUDA_TRY(cudaEventRecord(e->ev_level[lv], e->copy_stream));
       BI_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_level[lv], 0));
     } else if (lv < e->k) {
@@ -1527,6 +1611,7 @@ static int run_host_pipelined(bi_engine* e, const double* in, int64_t ld_in, int
     io.s_out = dst_s;
     int rc = run_impl(e, first, last, use_graph, s, io.out ? &io : nullptr);
     if (rc) return rc;
+    if (trace) fprintf(stderr, "[pipe] steps %d-%d enqueued (t=%.0f)\n", first, last, now_us() - t_start);
     done = last;
   }
   e->last_first = 1;
