@@ -485,8 +485,17 @@ def run_sharded_arm(args) -> None:
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BI_BENCH_SHARE_GPU=1 (harness self-test only, never a measurement): ranks
+    # share the visible GPUs and exchange over gloo (NCCL refuses two ranks on
+    # one GPU), so the N > 1 path can be exercised on a 1-GPU box
+    share = os.environ.get("BI_BENCH_SHARE_GPU") == "1"
+    if share:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if share:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2305_11103_b200 as bi  # noqa: F401  (after the build on local rank 0)
     from paper_2305_11103_b200.distributed import sharded_engine
     from paper_2305_11103_b200.workloads import cfg4
@@ -511,7 +520,7 @@ def run_sharded_arm(args) -> None:
         torch.cuda.synchronize()
         dist.barrier()
     eng.check()
-    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cpu" if share else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
     value = nominal_flops(N) / (ms_step * 1e-3) / 1e12
@@ -527,7 +536,7 @@ def run_sharded_arm(args) -> None:
         full = eng.gather(0)
         b.record(stream)
         torch.cuda.synchronize()
-        tt = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         if i:
             e2e.append(float(tt.item()))
@@ -552,6 +561,8 @@ def run_sharded_arm(args) -> None:
             "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
             "residual_fro": float(fro),
         }
+        if share:
+            line["harness_self_test"] = "BI_BENCH_SHARE_GPU=1: ranks share one GPU over gloo -- not a measurement"
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
@@ -563,7 +574,7 @@ def _self_launch(args, argv) -> int:
     import torch
 
     visible = torch.cuda.device_count()
-    if visible < args.gpus:
+    if visible < args.gpus and os.environ.get("BI_BENCH_SHARE_GPU") != "1":
         print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {visible}", file=sys.stderr)
         return 2
     s = socket.socket()
