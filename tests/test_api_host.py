@@ -154,3 +154,24 @@ def test_cli_parser_and_host_commands(tmp_path, capsys):
     assert cli.main(["partition", "1"]) == cli.EXIT_IO  # InvalidOrder
     with pytest.raises(SystemExit):
         cli.main(["invert", "--in", "x", "--method", "lu"])
+
+
+def test_file_block_store_roundtrip(tmp_path):
+    """FileBlockStore (storage.py:73-125): one BMAT file per block, region
+    reads/writes across block boundaries, BlockMatrix.from_dense(directory=)."""
+    scheme = bi.partition_from_sizes([3, 5, 2, 6])
+    g = np.random.default_rng(3)
+    m = g.standard_normal((16, 16))
+    bm = storage.BlockMatrix.from_dense(m, scheme, directory=tmp_path / "blocks")
+    assert isinstance(bm.store, storage.FileBlockStore) and bm.store.file_backed
+    assert sorted(p.name for p in (tmp_path / "blocks").glob("*.blk")) == sorted(
+        f"B_{i}_{j}.blk" for i in range(4) for j in range(4))
+    assert np.array_equal(bm.to_dense(), m)
+    off = scheme.offsets
+    assert np.array_equal(bm.store.region(1, 3, 0, 2), m[off[1]:off[3], off[0]:off[2]])
+    vals = g.standard_normal((off[3] - off[1], off[4] - off[2]))
+    bm.store.set_region(1, 3, 2, 4, vals)
+    m2 = m.copy()
+    m2[off[1]:off[3], off[2]:off[4]] = vals
+    assert np.array_equal(bm.to_dense(), m2)
+    assert np.array_equal(storage.FileBlockStore(scheme, tmp_path / "blocks").to_dense(), m2)  # reopened

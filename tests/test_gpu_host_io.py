@@ -127,3 +127,13 @@ def test_pageable_singular_reported(bi):
     # the engine stays usable afterwards
     good = well_conditioned(n, 10)
     assert oracle.residual_max(good, bi.run_inversion(good, sizes=sizes).to_dense()) <= 1e-8 * n
+
+
+def test_pageable_batch_more_lanes_than_streams(bi):
+    """batch 10 > 8 lanes: lanes carry two matrices; need-ordered staging
+    over every matrix of every level."""
+    sizes = [24] * 8
+    ms = _batch(sizes, 10, 70)
+    ref = _device_ref(bi, ms, sizes)
+    got = bi.run_inversion_batch(ms, sizes)
+    assert np.array_equal(got, ref)
