@@ -30,7 +30,7 @@ enum {
   BI_ESINGULAR = 1, /* a pivot block / Schur complement is singular      */
   BI_EDIM = 2,      /* shape / argument error (DimensionMismatch, ...)    */
   BI_ECUDA = 3,     /* CUDA runtime error                                 */
-  BI_ENCCL = 4,     /* collective error (reserved: multi-GPU scheduler)   */
+  BI_ENCCL = 4,     /* NCCL error / NCCL unavailable (multi-GPU transport) */
   BI_EUNSUPPORTED = 5
 };
 
@@ -221,6 +221,21 @@ int bi_engine_xchg_pack(bi_engine* e, int i, void* stream);
 int bi_engine_xchg_unpack(bi_engine* e, int i, void* stream);
 int bi_shard_group_run(bi_engine** engines, int nranks, void* const* streams, int first_step, int last_step,
                        int use_graph);
+/* Transport C, one process per GPU, NCCL inside the library (libnccl.so.2 is
+ * dlopen'ed; a process that already loaded NCCL shares it):
+ *   rank 0: bi_nccl_unique_id(id) -> every rank (out of band, e.g. a
+ *   torch.distributed broadcast) -> bi_nccl_comm_init(P, id, rank, &world)
+ *   on its GPU -> bi_engine_shard_set_comm(e, world) (collective: one
+ *   ncclCommSplit per power-of-two group size) -> bi_engine_run_nccl(e, 1,
+ *   N_s, use_graph, stream): every segment and every exchange (pack ->
+ *   ncclAllGather -> unpack) enqueued by this one call, stream-ordered.
+ * BI_ENCCL reports NCCL failures or a missing / too old libnccl. */
+int bi_nccl_available(void);
+int bi_nccl_unique_id(unsigned char* id /* 128 bytes */);
+int bi_nccl_comm_init(int nranks, const unsigned char* id, int rank, void** comm);
+int bi_nccl_comm_destroy(void* comm);
+int bi_engine_shard_set_comm(bi_engine* e, void* world_comm);
+int bi_engine_run_nccl(bi_engine* e, int first_step, int last_step, int use_graph, void* stream);
 /* Enqueue only one class of ops of steps [first, last] (no graph): mask 1 =
  * the engine's K1 GEMM launches, 2 = the leaf inversions (K3 incl. their
  * trailing-update GEMMs), 3 = both.  For per-kernel timing in bench.py. */

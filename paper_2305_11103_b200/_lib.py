@@ -65,6 +65,12 @@ SIGNATURES = [
     ("bi_engine_xchg_pack", _c_int, [_vp, _c_int, _vp]),
     ("bi_engine_xchg_unpack", _c_int, [_vp, _c_int, _vp]),
     ("bi_shard_group_run", _c_int, [ctypes.POINTER(_vp), _c_int, ctypes.POINTER(_vp), _c_int, _c_int, _c_int]),
+    ("bi_nccl_available", _c_int, []),
+    ("bi_nccl_unique_id", _c_int, [ctypes.c_char_p]),
+    ("bi_nccl_comm_init", _c_int, [_c_int, ctypes.c_char_p, _c_int, ctypes.POINTER(_vp)]),
+    ("bi_nccl_comm_destroy", _c_int, [_vp]),
+    ("bi_engine_shard_set_comm", _c_int, [_vp, _vp]),
+    ("bi_engine_run_nccl", _c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
     ("bi_schur2x2_workspace_bytes", _c_i64, [_c_i64, _c_i64]),
     ("bi_schur2x2", _c_int, [_c_int, _c_i64, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _pint, _vp]),
     ("bi_inplace_by_a_workspace_bytes", _c_i64, [_c_i64, _c_i64]),
@@ -83,6 +89,10 @@ class NativeUnavailable(BlockInvError, RuntimeError):
 
 class NativeError(BlockInvError, RuntimeError):
     """A CUDA/runtime failure reported by the native library."""
+
+
+class CollectiveError(NativeError):
+    """An NCCL failure (or a missing libnccl) in the multi-GPU transport."""
 
 
 _lib = None
@@ -121,6 +131,8 @@ def check(rc: int, what: str = "") -> int:
         raise DimensionMismatch(f"{what}: {msg}")
     if rc == BI_EUNSUPPORTED:
         raise NotImplementedError(f"{what}: {msg}")
+    if rc == BI_ENCCL:
+        raise CollectiveError(f"{what}: {msg}")
     raise NativeError(f"{what}: status {rc}: {msg}")
 
 

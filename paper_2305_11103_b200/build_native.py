@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 
-SOURCES = ["bi_gemm.cu", "bi_gemm_tma.cu", "bi_gemm_peer.cu", "bi_inv.cu", "bi_engine.cu", "bi_capi.cu"]
+SOURCES = ["bi_gemm.cu", "bi_gemm_tma.cu", "bi_gemm_peer.cu", "bi_inv.cu", "bi_engine.cu", "bi_capi.cu", "bi_nccl.cu"]
 
 
 def _deps() -> list[Path]:

@@ -37,6 +37,7 @@
 
 #include "../../include/blockinv_b200.h"
 #include "bi_common.cuh"
+#include "bi_shard_internal.cuh"
 
 namespace bi {
 
@@ -240,6 +241,7 @@ struct bi_engine {
   std::vector<FlatOp> flat;         // lane 0's ops of steps 1..N_s in order
   std::vector<int> step_first_op;   // [stepid] -> first index into flat (N_s + 2 entries)
   std::map<std::pair<int, int>, cudaGraphExec_t> seg_graphs;
+  std::map<int, void*> group_comms;  // NCCL transport: group size -> ncclComm_t (bi_nccl.cu)
   int device = 0;
   int* info = nullptr;
   GemmDesc* d_descs = nullptr;
@@ -1822,6 +1824,7 @@ extern "C" int bi_engine_tset_square(const bi_engine* e, int level, int quad, in
 }
 
 extern "C" int bi_engine_destroy(bi_engine* e) {
+  if (e && !e->group_comms.empty()) shard_destroy_comms(e);
   delete e;
   return 0;
 }
@@ -2073,3 +2076,15 @@ extern "C" int bi_shard_group_run(bi_engine** es, int P, void* const* streams, i
   cleanup();
   return 0;
 }
+
+namespace bi {
+bool shard_staging(const bi_engine* e) { return (e->shard_flags & BI_SHARD_STAGING) != 0; }
+int shard_nranks(const bi_engine* e) { return e->P; }
+int shard_rank(const bi_engine* e) { return e->rank; }
+std::map<int, void*>& shard_group_comms(bi_engine* e) { return e->group_comms; }
+int shard_zero_minv(bi_engine* e, cudaStream_t s) {
+  e->last_first = 1;
+  BI_CUDA_TRY(cudaMemset2DAsync(e->Minv, e->ldi * 8, 0, e->w * 8, e->n, s));
+  return 0;
+}
+}  // namespace bi

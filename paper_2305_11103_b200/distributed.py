@@ -550,9 +550,27 @@ class NativeShardDist:
         self.group = group if group is not None else dist.group.WORLD
         P, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
         self.shard = NativeShard(sizes, P, rank, staging=True)
-        self.groups = make_groups(dist, P, self.group)
         self.P, self.rank, self.n = P, rank, self.shard.n
         self._last = self.shard.n_steps
+        # BI_SHARD_TRANSPORT=lib: the exchanges as NCCL calls inside the
+        # library (one C call per run); default: torch.distributed collectives
+        import os
+
+        self.lib = None
+        if os.environ.get("BI_SHARD_TRANSPORT") == "lib" and dist.get_backend(self.group) == "nccl":
+            from .shard import LibNccl
+
+            def share_id(raw: bytes) -> bytes:
+                box = [raw]
+                dist.broadcast_object_list(box, src=dist.get_global_rank(self.group, 0)
+                                           if self.group is not dist.group.WORLD else 0, group=self.group)
+                return box[0]
+
+            self.lib = LibNccl(P, rank, share_id)
+            self.lib.attach(self.shard)
+            self.groups = {}
+        else:
+            self.groups = make_groups(dist, P, self.group)
 
     def load(self, m) -> None:
         self.shard.load(m)
@@ -561,7 +579,10 @@ class NativeShardDist:
         nsteps = self.shard.n_steps
         last = nsteps if last is None else max(first, min(int(last), nsteps))
         self._last = last
-        self.shard.run_dist(self.dist, self.groups, first, last)
+        if self.lib is not None:
+            self.lib.run(self.shard, first, last)
+        else:
+            self.shard.run_dist(self.dist, self.groups, first, last)
 
     def check(self) -> None:
         """SingularBlock(step, quad) of the earliest singular leaf on any rank (collective)."""

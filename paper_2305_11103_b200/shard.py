@@ -166,6 +166,37 @@ class NativeShard:
             _lib.check(L.bi_engine_xchg_unpack(self._h, xi, st), "bi_engine_xchg_unpack")
 
 
+class LibNccl:
+    """Transport C: NCCL inside the library (bi_nccl.cu).  The world
+    communicator is created from a unique id that rank 0 draws and
+    ``exchange_id`` hands to every rank (e.g. a torch.distributed
+    broadcast); ``attach`` splits the group communicators of a shard."""
+
+    def __init__(self, nranks: int, rank: int, exchange_id):
+        L = _lib.lib()
+        if not L.bi_nccl_available():
+            raise _lib.CollectiveError("libnccl.so.2 is not loadable: no in-library NCCL transport")
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _lib.check(L.bi_nccl_unique_id(uid), "bi_nccl_unique_id")
+        uid = exchange_id(bytes(uid.raw))
+        self.comm = _lib._vp()
+        _lib.check(L.bi_nccl_comm_init(int(nranks), uid, int(rank), ctypes.byref(self.comm)), "bi_nccl_comm_init")
+
+    def attach(self, shard: "NativeShard") -> None:
+        _lib.check(_lib.lib().bi_engine_shard_set_comm(shard._h, self.comm), "bi_engine_shard_set_comm")
+
+    def run(self, shard: "NativeShard", first: int = 1, last: int | None = None, use_graph: bool = True) -> None:
+        last = shard.n_steps if last is None else last
+        _lib.check(_lib.lib().bi_engine_run_nccl(shard._h, first, last, 1 if use_graph else 0, _lib.stream_ptr()),
+                   "bi_engine_run_nccl")
+
+    def close(self) -> None:
+        if self.comm.value:
+            _lib.lib().bi_nccl_comm_destroy(self.comm)
+            self.comm = _lib._vp()
+
+
 def make_groups(dist, nranks: int, group=None) -> dict:
     """Every power-of-two rank group of the level scheduler, created
     collectively in the same order on every rank: {(size, first rank): pg}."""

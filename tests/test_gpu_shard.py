@@ -119,3 +119,30 @@ def test_plan_matches_python_scheduler(bi):
             gs = (1 << x["level"]) // nbp
             assert x["gs"] == gs and x["g0"] == r // gs * gs
             assert x["in_a"] == (r - x["g0"] < gs // 2)
+
+
+def test_library_nccl_transport_single_rank(bi):
+    """Transport C (NCCL inside the library, bi_nccl.cu) on one rank: the
+    dlopen'ed libnccl, a 1-rank world communicator, bi_engine_run_nccl over
+    every segment -- bitwise equal to the single engine.  (Ranks > 1 need
+    one GPU each: NCCL refuses two ranks on one device.)"""
+    from paper_2305_11103_b200 import _lib
+    from paper_2305_11103_b200.shard import LibNccl, NativeShard
+
+    if not _lib.lib().bi_nccl_available():
+        pytest.skip("libnccl.so.2 not loadable")
+    sizes = [48] * 8
+    n = sum(sizes)
+    m = well_conditioned(n, 31)
+    sh = NativeShard(sizes, 1, 0, staging=True)
+    sh.load(m)
+    tr = LibNccl(1, 0, lambda raw: raw)
+    try:
+        tr.attach(sh)
+        tr.run(sh)
+        assert sh.check() is None
+        out = np.empty((n, n))
+        sh.write_slab(out)
+    finally:
+        tr.close()
+    assert np.array_equal(out, bi.run_inversion(m, sizes=sizes).to_dense())
