@@ -6,8 +6,8 @@ residual ||A X - I||_F (K1 + K4).
   cfg3  n=6000, split 1000, singular A11: invert_with_fallback -> via_d
   cfg4  n=16384, 64 x 256 blocks: run_inversion step engine (127 steps)
   cfg5  n=65536, 256 x 256 blocks (--cfg5): run_inversion on ONE GPU
-        (~138 GB of device state); input drawn on the device (torch
-        Philox, seed 5) with the config's distribution, N(0,1)/256 + 4I
+        (~138 GB of device state); the config's own seed-5 NumPy stream
+        (workloads.cfg5), plus one end-to-end run_inversion on the NumPy array
   cfg4 and cfg5 also run the opt-in schedule="pivot_a" (2n^3 block-level
   invertor_by_a recursion).
 """
@@ -111,31 +111,30 @@ def main():
             torch.cuda.empty_cache()
         del m
 
-    for sched in (("eq7", "pivot_a") if args.cfg5 else ()):
+    if args.cfg5:
         n = 65536
-        sizes = [256] * 256
-        torch.cuda.reset_peak_memory_stats()
-        eng = bi.DeviceEngine(sizes, 1, schedule=sched)
-        g = torch.Generator(device="cuda")
-        g.manual_seed(5)
-        for r0 in range(0, n, 4096):  # draw row chunks straight into M
-            blk = torch.randn((4096, n), generator=g, dtype=torch.float64, device="cuda")
-            blk.div_(256.0)
-            eng.M[0, r0:r0 + 4096].copy_(blk)
-            del blk
-        idx = torch.arange(n, device="cuda")
-        eng.M[0, idx, idx] += 4.0
-        torch.cuda.synchronize()
-        ms = time_engine(eng, 1)
-        fro, mx = _residual_device(eng.M, eng.Minv, batch=True)
-        key = "cfg5" if sched == "eq7" else "cfg5_pivot_a"
-        out[key] = {"run_inversion_device_s": ms / 1e3, "tflops_nominal": 2 * n**3 / (ms * 1e-3) / 1e12,
-                    "residual_fro": float(fro[0]), "residual_max": float(mx[0]),
-                    "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9, "schedule": sched,
-                    "input": "device-drawn N(0,1)/256 + 4I (torch Philox, seed 5)"}
-        print(key, out[key], flush=True)
-        del eng
-        torch.cuda.empty_cache()
+        m5, sizes = workloads.cfg5()  # the config's own seed-5 NumPy stream, 34 GB
+        for sched in ("eq7", "pivot_a"):
+            torch.cuda.reset_peak_memory_stats()
+            eng = bi.DeviceEngine(sizes, 1, schedule=sched)
+            eng.load(m5)
+            torch.cuda.synchronize()
+            ms = time_engine(eng, 1)
+            fro, mx = _residual_device(eng.M, eng.Minv, batch=True)
+            key = "cfg5" if sched == "eq7" else "cfg5_pivot_a"
+            out[key] = {"run_inversion_device_s": ms / 1e3, "tflops_nominal": 2 * n**3 / (ms * 1e-3) / 1e12,
+                        "residual_fro": float(fro[0]), "residual_max": float(mx[0]),
+                        "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9, "schedule": sched,
+                        "input": "workloads.cfg5(): N(0,1)/256 + 4I from numpy default_rng(5)"}
+            print(key, out[key], flush=True)
+            del eng
+            bi.release_engines()
+        t0 = time.perf_counter()
+        x = bi.run_inversion(m5, sizes=sizes).store.data  # end to end, NumPy in / NumPy out
+        out["cfg5_e2e_s"] = time.perf_counter() - t0
+        print("cfg5 e2e run_inversion", out["cfg5_e2e_s"], "s", flush=True)
+        del x
+        bi.release_engines()
     print(json.dumps(out))
 
 
