@@ -279,11 +279,21 @@ struct bi_engine {
   double* stage_out = nullptr;
   int64_t stage_in_bytes = 0, stage_out_bytes = 0;
   cudaEvent_t ev_level[32] = {};  // H2D of input level l done (pipelined host path)
+  // bounded page-locked ring for host buffers above the staging limit
+  static constexpr int kRingSlots = 4;
+  int64_t ring_bytes = 0;  // slot size: 256 MB (BI_RING_MB overrides; tests use tiny slots)
+  char* ring[kRingSlots] = {};
+  cudaEvent_t ring_ev[kRingSlots] = {};
+  bool ring_busy[kRingSlots] = {};
 
   ~bi_engine() {
     for (auto& kv : seg_graphs) cudaGraphExecDestroy(kv.second);
     if (stage_in) cudaFreeHost(stage_in);
     if (stage_out) cudaFreeHost(stage_out);
+    for (int i = 0; i < kRingSlots; ++i) {
+      if (ring[i]) cudaFreeHost(ring[i]);
+      if (ring_ev[i]) cudaEventDestroy(ring_ev[i]);
+    }
     for (cudaEvent_t ev : ev_level)
       if (ev) cudaEventDestroy(ev);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
@@ -1629,6 +1639,159 @@ static int run_host_pipelined(bi_engine* e, const double* in, int64_t ld_in, int
   return 0;
 }
 
+// Host buffers above the staging limit (cfg5: 34 GB each way): the same
+// need-ordered level pipeline through a bounded page-locked ring (4 x 256 MB)
+// -- the host packs pieces into a slot (all host threads), the copy stream
+// DMAs the slot, and a slot is refilled once its DMA event has fired.  The
+// inverse comes back through the same ring after the run (DMA of chunk i+1
+// under the host copy of chunk i).
+static int run_host_ring(bi_engine* e, const double* in, int64_t ld_in, int64_t s_in, double* out,
+                         int64_t ld_out, int64_t s_out, int last_step, int use_graph, cudaStream_t s) {
+  constexpr int R = bi_engine::kRingSlots;
+  if (!e->ring_bytes) {
+    const char* v = getenv("BI_RING_MB");
+    e->ring_bytes = (int64_t)((v ? atof(v) : 256.0) * (1 << 20));
+    e->ring_bytes = std::max<int64_t>(round_up(e->ring_bytes, 256), 256);
+  }
+  const int64_t RB = e->ring_bytes;
+  const int64_t n = e->n;
+  const int T = host_threads();
+  for (int i = 0; i < R; ++i) {
+    if (!e->ring[i]) BI_CUDA_TRY(cudaHostAlloc((void**)&e->ring[i], RB, cudaHostAllocPortable));
+    if (!e->ring_ev[i]) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ring_ev[i], cudaEventDisableTiming));
+    e->ring_busy[i] = false;
+  }
+  for (int lv = 0; lv <= e->k; ++lv)
+    if (!e->ev_level[lv]) BI_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_level[lv], cudaEventDisableTiming));
+  for (int z = 0; z < e->Z; ++z)
+    BI_CUDA_TRY(cudaMemset2DAsync(e->Minv + (int64_t)z * e->si, e->ldi * 8, 0, n * 8, n, s));
+  const bool in_pinned = is_pinned(in), out_pinned = is_pinned(out);
+  int slot = 0;
+  int64_t fill = 0;
+  struct Q {
+    char* dev;
+    int64_t dld, off, rows, bytes;
+  };
+  std::vector<Q> queued;
+  std::vector<Region> regs;
+  auto flush = [&]() -> cudaError_t {
+    if (queued.empty()) return cudaSuccess;
+    par_copy(regs, T);  // host rows -> the slot
+    regs.clear();
+    for (const Q& q : queued) {
+      cudaError_t err = cudaMemcpy2DAsync(q.dev, q.dld, e->ring[slot] + q.off, q.bytes, q.bytes, q.rows,
+                                          cudaMemcpyHostToDevice, e->copy_stream);
+      if (err != cudaSuccess) return err;
+    }
+    queued.clear();
+    cudaError_t err = cudaEventRecord(e->ring_ev[slot], e->copy_stream);
+    e->ring_busy[slot] = true;
+    slot = (slot + 1) % R;
+    fill = 0;
+    if (err == cudaSuccess && e->ring_busy[slot]) err = cudaEventSynchronize(e->ring_ev[slot]);  // slot free again
+    e->ring_busy[slot] = false;
+    return err;
+  };
+  auto stage = [&](const char* host, int64_t hld, int64_t rows, int64_t bytes, char* dev, int64_t dld) -> cudaError_t {
+    for (int64_t r = 0; r < rows;) {
+      const int64_t fit = fill >= RB ? 0 : (RB - fill) / bytes;
+      if (fit <= 0) {
+        cudaError_t err = flush();
+        if (err != cudaSuccess) return err;
+        if (RB / bytes == 0) return cudaErrorInvalidValue;  // a row larger than a slot
+        continue;
+      }
+      const int64_t take = std::min(fit, rows - r);
+      regs.push_back({e->ring[slot] + fill, host + r * hld, bytes, hld, take, bytes});
+      queued.push_back({dev + r * dld, dld, fill, take, bytes});
+      fill += round_up(take * bytes, 256);
+      r += take;
+    }
+    return cudaSuccess;
+  };
+  std::vector<std::array<int, 4>> blocks;
+  int done = 0;
+  for (int lv = 0; lv <= e->k; ++lv) {
+    if (in) {
+      level_blocks(e, lv, blocks);
+      for (int z = 0; z < e->Z; ++z)
+        for (const auto& b : blocks) {
+          const int64_t ro = e->off[b[0]], co = e->off[b[2]], rows = e->off[b[1]] - ro, bytes = (e->off[b[3]] - co) * 8;
+          const double* h = in + (int64_t)z * s_in + ro * ld_in + co;
+          double* d = const_cast<double*>(e->M) + (int64_t)z * e->sm + ro * e->ldm + co;
+          if (in_pinned) {
+            BI_CUDA_TRY(cudaMemcpy2DAsync(d, e->ldm * 8, h, ld_in * 8, bytes, rows, cudaMemcpyHostToDevice,
+                                          e->copy_stream));
+          } else {
+            BI_CUDA_TRY(stage((const char*)h, ld_in * 8, rows, bytes, (char*)d, e->ldm * 8));
+          }
+        }
+      BI_CUDA_TRY(flush());
+      BI_CUDA_TRY(cudaEventRecord(e->ev_level[lv], e->copy_stream));
+      BI_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_level[lv], 0));
+    } else if (lv < e->k) {
+      continue;
+    }
+    if (done >= last_step) continue;
+    int first = done + 1, last;
+    if (e->schedule == BI_SCHEDULE_PIVOT_A) {
+      if (in && lv < e->k) continue;
+      last = 1;
+    } else {
+      last = lv == e->k || !in ? e->nsteps : (1 << (lv + 1)) - 1;
+    }
+    last = std::min(last, last_step);
+    int rc = run_impl(e, first, last, use_graph, s, nullptr);
+    if (rc) return rc;
+    done = last;
+  }
+  e->last_first = 1;
+  e->last_last = last_step;
+  if (!out) return 0;
+  // read-back: after the run, M_inv rows in ring-sized chunks
+  BI_CUDA_TRY(cudaEventRecord(e->ev_fork, s));
+  BI_CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, e->ev_fork, 0));
+  if (out_pinned) {
+    for (int z = 0; z < e->Z; ++z)
+      BI_CUDA_TRY(cudaMemcpy2DAsync(out + (int64_t)z * s_out, ld_out * 8, e->Minv + (int64_t)z * e->si, e->ldi * 8,
+                                    n * 8, n, cudaMemcpyDeviceToHost, e->copy_stream));
+    BI_CUDA_TRY(cudaEventRecord(e->ev_fork, e->copy_stream));
+    BI_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_fork, 0));
+    return 0;
+  }
+  const int64_t rows_per = std::max<int64_t>(1, RB / (n * 8));
+  struct C {
+    int z;
+    int64_t r0, rows;
+    int slot;
+  };
+  std::vector<C> inflight;
+  int sl = 0;
+  auto drain_one = [&]() -> cudaError_t {
+    const C c = inflight.front();
+    inflight.erase(inflight.begin());
+    cudaError_t err = cudaEventSynchronize(e->ring_ev[c.slot]);
+    if (err != cudaSuccess) return err;
+    std::vector<Region> rg{{(char*)(out + (int64_t)c.z * s_out + c.r0 * ld_out), e->ring[c.slot], ld_out * 8, n * 8,
+                            c.rows, n * 8}};
+    par_copy(rg, T);
+    return cudaSuccess;
+  };
+  for (int z = 0; z < e->Z; ++z)
+    for (int64_t r0 = 0; r0 < n; r0 += rows_per) {
+      if ((int)inflight.size() == R) BI_CUDA_TRY(drain_one());
+      const int64_t rows = std::min(rows_per, n - r0);
+      BI_CUDA_TRY(cudaMemcpy2DAsync(e->ring[sl], n * 8, e->Minv + (int64_t)z * e->si + r0 * e->ldi, e->ldi * 8,
+                                    n * 8, rows, cudaMemcpyDeviceToHost, e->copy_stream));
+      BI_CUDA_TRY(cudaEventRecord(e->ring_ev[sl], e->copy_stream));
+      inflight.push_back({z, r0, rows, sl});
+      sl = (sl + 1) % R;
+    }
+  while (!inflight.empty()) BI_CUDA_TRY(drain_one());
+  for (int i = 0; i < R; ++i) e->ring_busy[i] = false;
+  return 0;
+}
+
 extern "C" int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t ld_in, int64_t stride_in,
                                   double* host_out, int64_t ld_out, int64_t stride_out, int first_step,
                                   int last_step, int use_graph, void* stream) {
@@ -1646,10 +1809,13 @@ extern "C" int bi_engine_run_host(bi_engine* e, const double* host_in, int64_t l
     const char* v = getenv("BI_STAGE_LIMIT_GB");
     return (int64_t)((v ? atof(v) : 8.0) * (1 << 30));
   }();
-  if (((host_in && !is_pinned(host_in)) || (host_out && !is_pinned(host_out))) && stage_bytes <= stage_limit &&
-      first_step == 1)
-    return run_host_pipelined(e, host_in, ld_in, stride_in, host_out, ld_out, stride_out, last_step, use_graph,
-                              static_cast<cudaStream_t>(stream));
+  if (((host_in && !is_pinned(host_in)) || (host_out && !is_pinned(host_out))) && first_step == 1) {
+    if (stage_bytes <= stage_limit)
+      return run_host_pipelined(e, host_in, ld_in, stride_in, host_out, ld_out, stride_out, last_step, use_graph,
+                                static_cast<cudaStream_t>(stream));
+    return run_host_ring(e, host_in, ld_in, stride_in, host_out, ld_out, stride_out, last_step, use_graph,
+                         static_cast<cudaStream_t>(stream));
+  }
   HostIO io{host_in, ld_in, stride_in, host_out, ld_out, stride_out};
   return run_impl(e, first_step, last_step, use_graph, static_cast<cudaStream_t>(stream), &io);
 }

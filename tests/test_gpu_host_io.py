@@ -137,3 +137,43 @@ def test_pageable_batch_more_lanes_than_streams(bi):
     ref = _device_ref(bi, ms, sizes)
     got = bi.run_inversion_batch(ms, sizes)
     assert np.array_equal(got, ref)
+
+
+_RING_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2305_11103_b200 as bi
+from conftest import well_conditioned
+for sizes, batch in (([64] * 8, 1), ([37, 29, 51, 16, 44, 23, 60, 8], 3), ([128] * 16, 2)):
+    n = sum(sizes)
+    ms = np.stack([well_conditioned(n, 90 + b) for b in range(batch)])
+    eng = bi.DeviceEngine(sizes, batch=batch)
+    eng.load(ms); eng.run(); eng.check()
+    ref = eng.Minv[:, :, :n].cpu().numpy()
+    out = np.full_like(ms, np.nan)
+    eng.run_host(ms, out); eng.check()
+    assert np.array_equal(out, ref), sizes
+    for stop in (1, 4):
+        e2 = bi.DeviceEngine(sizes, batch=batch); e2.load(ms); e2.run(1, stop); e2.check()
+        o2 = np.full_like(ms, np.nan); eng.run_host(ms, o2, 1, stop); eng.check()
+        assert np.array_equal(o2, e2.Minv[:, :, :n].cpu().numpy()), (sizes, stop)
+print("ring ok")
+"""
+
+
+def test_ring_path_for_buffers_above_the_staging_limit(tmp_path):
+    """Host buffers above BI_STAGE_LIMIT_GB go through the bounded page-locked
+    ring (run_host_ring): forced here with a tiny limit and 64 KB slots so
+    pieces split across slots and every slot is reused many times."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, BI_STAGE_LIMIT_GB="1e-6", BI_RING_MB="0.0625",
+               PYTHONPATH=os.pathsep.join([str(root), str(root / "tests")]))
+    script = tmp_path / "ring.py"
+    script.write_text(_RING_SCRIPT)
+    r = subprocess.run([sys.executable, str(script), str(root)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ring ok" in r.stdout, r.stdout + r.stderr
