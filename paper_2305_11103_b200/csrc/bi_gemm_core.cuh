@@ -82,6 +82,32 @@ __device__ __forceinline__ void k1_compute(const uint8_t* stage, const K1Frag& f
   }
 }
 
+// The same k-tile on a 64 x 32 warp tile (rows wm*64 .. +63): the two 32-row
+// halves are exactly the 32 x 32 tiles (2wm, wn) and (2wm+1, wn) of
+// k1_compute, with the same fragments and k-step order per accumulator --
+// bitwise the same sums -- but each B fragment feeds 8 DMMAs instead of 4
+// (0.375 instead of 0.5 shared loads per DMMA, half the warps per SM).
+template <int StageA = kK1StageA>
+__device__ __forceinline__ void k1_compute_64x32(const uint8_t* stage, const K1Frag& f, int wm, int wn, int fr,
+                                                 double (&acc)[2][4][4][2]) {
+  const uint8_t* sa = stage + (wm * 64 + fr) * 128;
+  const uint8_t* sb = stage + StageA + (wn * 2) * kK1BoxB;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    double af[8], bf[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) af[i] = *reinterpret_cast<const double*>(sa + i * 8 * 128 + f.aoff[s]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * kK1BoxB + f.boff[s][j & 1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) k1_dmma(acc[h][i][j], af[4 * h + i], bf[j]);
+  }
+}
+
 // D = [C] + sign * acc with the output column remap; all C loads before any
 // D store (C may alias D).  Every C load of the thread is issued before the
 // first use, so the 16 loads overlap instead of paying one L2/DRAM latency

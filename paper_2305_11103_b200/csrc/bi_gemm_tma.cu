@@ -41,6 +41,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -183,9 +184,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_cons
 // slowest warp, and the next tile's first loads overlap this tile's tail.
 // TN = 128: 16 warps, one CTA per SM.  TN = 64: 8 warps on a 128 x 64 tile,
 // two CTAs per SM, so one CTA's epilogue runs under the other's main loop.
-template <int TN>
+// Fat = true: 4 warps of 64 x 32 on the 128 x 64 tile (k1_compute_64x32),
+// the shape cuBLAS's DGEMM uses on sm_100 (ncu: 128 threads, 220 registers,
+// two CTAs per SM); same summation order as the 8-warp tile.
+template <int TN, bool Fat = false>
 struct RefillCfg {
-  static constexpr int kWarpsT = 4 * (TN / 32);
+  static constexpr int kWarpsT = Fat ? 4 : 4 * (TN / 32);
   static constexpr int kThr = kWarpsT * 32;
   static constexpr int kStageB = kBK * TN * 8;
   static constexpr int kStage = kStageA + kStageB;
@@ -194,18 +198,18 @@ struct RefillCfg {
 template <int kStages, int TN>
 constexpr int refill_smem() { return kStages * RefillCfg<TN>::kStage + 1024; }
 
-template <int kStages, int TN>
-__global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks)
+template <int kStages, int TN, bool Fat = false>
+__global__ void __launch_bounds__(RefillCfg<TN, Fat>::kThr, RefillCfg<TN, Fat>::kMinBlocks)
     gemm_tma_refill_kernel(const __grid_constant__ TmaLaunch L) {
   pdl_enter();
-  using Cfg = RefillCfg<TN>;
+  using Cfg = RefillCfg<TN, Fat>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ unsigned released[kStages];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = warp / (TN / 32), wn = warp % (TN / 32);
+  const int wm = Fat ? warp >> 1 : warp / (TN / 32), wn = Fat ? warp & 1 : warp % (TN / 32);
   const int fr = lane >> 2, fc = lane & 3;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -248,16 +252,23 @@ __global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks
     const K1Tile tc = k1_locate<kBM, TN>(L.d, L.count, tile);
     const GemmDesc& d = L.d[tc.desc];
     const int KT = (d.K + kBK - 1) / kBK;
-    double acc[4][4][2];
+    constexpr int H = Fat ? 2 : 1;  // 32-row halves of the warp tile
+    double acc[H][4][4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int h = 0; h < H; ++h)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[h][i][j][0] = acc[h][i][j][1] = 0.0;
 
     for (int kt = 0; kt < KT; ++kt) {
       const int stage = cons_it % kStages;
       mbar_wait(&full[stage], (cons_it / kStages) & 1);
-      k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
+      if constexpr (Fat) {
+        k1_compute_64x32<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
+      } else {
+        k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc[0]);
+      }
       __syncwarp();
       if (lane == 0 && release_stage(&released[stage], Cfg::kWarpsT)) {
         released[stage] = 0;
@@ -266,7 +277,8 @@ __global__ void __launch_bounds__(RefillCfg<TN>::kThr, RefillCfg<TN>::kMinBlocks
       ++cons_it;
     }
 
-    k1_epilogue<kBM, TN>(d, tc.bz, tc.m0, tc.n0, wm, wn, fr, fc, acc);
+#pragma unroll
+    for (int h = 0; h < H; ++h) k1_epilogue<kBM, TN>(d, tc.bz, tc.m0, tc.n0, H * wm + h, wn, fr, fc, acc[h]);
   }
 }
 
@@ -531,6 +543,10 @@ cudaError_t tma_init() {
       e = cudaFuncSetAttribute(gemm_tma_refill_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                refill_smem<4, 64>());
     if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_tma_refill_kernel<4, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               refill_smem<4, 64>());
+    if (e == cudaSuccess) e = set_carveout(gemm_tma_refill_kernel<4, 64, true>);
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_tma_kseg_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                refill_smem<4, 64>());
     if (e == cudaSuccess) e = set_carveout(gemm_tma_kseg_kernel<4, 64>);
@@ -657,8 +673,25 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
     L.total_tiles = t;
     const int cap2 = grid_cap > 0 ? 2 * grid_cap : 0;
     const int grid2 = (cap2 > 0 && cap2 < t) ? cap2 : t;
-    *err = launch_kernel(gemm_tma_refill_kernel<4, 64>, dim3(grid2), dim3(RefillCfg<64>::kThr),
-                         (size_t)refill_smem<4, 64>(), stream, 1u, L);
+    // BI_GEMM_WARPS: 8 = 32 x 32 warp tiles, 4 = 64 x 32 (the cuBLAS shape),
+    // unset = 4 when every descriptor has K >= 1024.  Measured (tools/gemm_sweep.py,
+    // profiles/r02_k1_fat_warps.txt): 4 warps win on long k loops (8192^3 34.50 ->
+    // 35.41 TF/s, cuBLAS 35.48; 1024^3 x 16 33.93 -> 34.30) and lose on short ones
+    // (512^3 x 32 32.8 -> 28.8; K3's K = 128 updates 22.5 -> 18.6), where fewer
+    // warps per CTA hide less of each tile's prologue and epilogue.
+    static const int warps_env = [] {
+      const char* e = getenv("BI_GEMM_WARPS");
+      return e ? atoi(e) : 0;
+    }();
+    int kmin = INT32_MAX;
+    for (int i = 0; i < count; ++i) kmin = std::min(kmin, L.d[i].K);
+    const bool fat = warps_env == 4 || (warps_env != 8 && kmin >= 1024);
+    if (fat)
+      *err = launch_kernel(gemm_tma_refill_kernel<4, 64, true>, dim3(grid2), dim3(RefillCfg<64, true>::kThr),
+                           (size_t)refill_smem<4, 64>(), stream, 1u, L);
+    else
+      *err = launch_kernel(gemm_tma_refill_kernel<4, 64>, dim3(grid2), dim3(RefillCfg<64>::kThr),
+                           (size_t)refill_smem<4, 64>(), stream, 1u, L);
     return true;
   }
   if (refill) {

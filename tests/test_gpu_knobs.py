@@ -8,6 +8,7 @@ import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -49,6 +50,11 @@ KNOBS = [
     {"BI_GEMM_TMA": "0", "BI_GEMM_CP_TN": "128"},
     {"BI_GEMM_TN": "128", "BI_GEMM_REFILL": "0"},
     {"BI_PRIORITY_MODE": "4", "BI_ENGINE_SKEW": "1", "BI_RESERVE_SMS": "16"},
+    {"BI_GJ_FUSED": "1"},
+    {"BI_GJ_FUSED": "1", "BI_GJ_FAST": "0"},
+    {"BI_GJ_FAST_SMALL": "1"},
+    {"BI_GEMM_WARPS": "4"},
+    {"BI_GEMM_WARPS": "8"},
 ]
 
 
@@ -58,3 +64,52 @@ def test_knob_combination_correct(knobs):
     r = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT)], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
+
+
+BITWISE_GEMM = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+from paper_2305_11103_b200 import _lib
+L = _lib.lib()
+g = torch.Generator(device="cuda").manual_seed(5)
+outs = []
+for m, n, k, batch, acc in ((1024, 1024, 1024, 2, True), (640, 200, 1100, 3, False), (2048, 512, 4096, 1, True),
+                            (300, 300, 300, 2, True)):
+    a = torch.randn(batch, m, k, dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn(batch, k, n, dtype=torch.float64, device="cuda", generator=g)
+    c = torch.randn(batch, m, n, dtype=torch.float64, device="cuda", generator=g) if acc else None
+    d = torch.empty(batch, m, n, dtype=torch.float64, device="cuda")
+    rc = L.bi_gemm(m, n, k, 1, a.data_ptr(), k, m * k, b.data_ptr(), n, k * n,
+                   c.data_ptr() if acc else None, n if acc else 0, m * n if acc else 0,
+                   d.data_ptr(), n, m * n, batch, _lib.stream_ptr())
+    assert rc == 0
+    outs.append(d.cpu().numpy())
+np.savez(sys.argv[2], *outs)
+print("ok")
+"""
+
+
+def test_gemm_warp_tiles_bitwise(tmp_path):
+    """K1's 4-warp (64 x 32) and 8-warp (32 x 32) tiles sum every element in the
+    same order: bitwise equal outputs, including ragged shapes."""
+    res = {}
+    for w in ("4", "8"):
+        f = tmp_path / f"w{w}.npz"
+        env = dict(os.environ, BI_GEMM_WARPS=w)
+        r = subprocess.run([sys.executable, "-c", BITWISE_GEMM, str(ROOT), str(f)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        res[w] = np.load(f)
+    for key in res["4"].files:
+        assert np.array_equal(res["4"][key], res["8"][key]), key
+
+
+def test_fused_small_inverter_bitwise():
+    """BI_GJ_FUSED=1 (one cluster launch per batch of blocks <= 512) is bitwise
+    the multi-launch chain, on dominant, random, permuted, singular, ragged and
+    tied blocks (tools/k3_fast_check.py)."""
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "k3_fast_check.py"), "BI_GJ_FUSED"], capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and "ALL BITWISE EQUAL" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]

@@ -1,8 +1,10 @@
-"""BI_GJ_FAST=1 (verified diagonal-pivot panels) against BI_GJ_FAST=0 (the
-pivoted column loop): bitwise equal inverses and info, on diagonally
-dominant blocks (fast path taken), random blocks (fallback), singular and
-permuted blocks, batches and a large cluster-panel block.
-    python tools/k3_fast_check.py            # driver: runs both modes, compares
+"""A K3 knob at 1 against 0, bitwise: BI_GJ_FAST=1 (verified diagonal-pivot
+panels) against the pivoted column loop, or BI_GJ_FUSED=1 (the fused
+single-launch cluster kernel for n <= 512) against the multi-launch chain.
+Inverses and info must be bitwise equal on diagonally dominant blocks (fast
+path taken), random blocks (fallback), singular and permuted blocks,
+batches, ragged orders and a large cluster-panel block.
+    python tools/k3_fast_check.py [KNOB]     # driver: runs both modes, compares
 """
 import os
 import subprocess
@@ -14,7 +16,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 CASES = [("dom", 64, 256), ("dom", 8, 512), ("rand", 8, 256), ("rand", 4, 512), ("perm", 4, 256),
          ("sing", 4, 256), ("dom", 1, 5000), ("rand", 1, 3000), ("dom", 3, 100), ("mixed", 16, 200),
-         ("dom", 1, 1000), ("tie", 2, 64)]
+         ("dom", 1, 1000), ("tie", 2, 64), ("dom", 2, 300), ("perm", 2, 512), ("dom", 3, 129), ("rand", 3, 24),
+         ("sing", 2, 512), ("rand", 2, 384)]
 
 
 def make(kind, cnt, n, seed):
@@ -51,15 +54,17 @@ def child(out_dir):
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1:
+    if len(sys.argv) > 1 and not sys.argv[1].startswith("BI_"):
         child(sys.argv[1])
         sys.exit(0)
     import tempfile
 
+    knob = sys.argv[1] if len(sys.argv) > 1 else "BI_GJ_FAST"
+    print(f"{knob}=0 vs {knob}=1")
     outs = {}
     for mode in ("0", "1"):
         d = tempfile.mkdtemp()
-        env = dict(os.environ, BI_GJ_FAST=mode)
+        env = dict(os.environ, **{knob: mode})
         subprocess.run([sys.executable, __file__, d], env=env, check=True)
         outs[mode] = d
     ok = True
