@@ -1053,6 +1053,16 @@ static int leaf_gemm_cap() {
   return cap;
 }
 
+// BI_ENGINE_PDL (default 0): measured within noise (cfg4 394.6 / 396.3 ms off,
+// 395.3 / 394.7 on; cfg2 27.0 / 26.9 vs 26.7 / 26.9; profiles/r02_k1_tiles.txt)
+static int engine_pdl() {
+  static const int on = [] {
+    const char* v = getenv("BI_ENGINE_PDL");
+    return v ? atoi(v) : 0;
+  }();
+  return on;
+}
+
 static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cudaStream_t s, int mask,
                                 cudaEvent_t after_first = nullptr, bool wait_input = false,
                                 const HostIO* split_io = nullptr) {
@@ -1109,6 +1119,11 @@ static cudaError_t enqueue_lane(bi_engine* e, int lane, int first, int last, cud
         err = pass_in_chunks(e, lane, e->launches[op.index], split_io, s);
       } else {
         GemmCapScope cap(e->gemm_cap);
+        // programmatic dependent launch between consecutive engine kernels: the
+        // next GEMM's CTAs are placed (and run their prologue) during the
+        // previous kernel's tail; griddepcontrol.wait in every kernel keeps the
+        // data dependency (BI_ENGINE_PDL, default 1)
+        PdlScope pdl(engine_pdl());
         const GemmLaunchRec& L = e->launches[op.index];
         err = launch_gemm(e->descs.data() + L.first, e->d_descs + L.first, L.count, s);
       }

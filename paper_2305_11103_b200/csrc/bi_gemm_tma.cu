@@ -187,22 +187,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const __grid_cons
 // Fat = true: 4 warps of 64 x 32 on the 128 x 64 tile (k1_compute_64x32),
 // the shape cuBLAS's DGEMM uses on sm_100 (ncu: 128 threads, 220 registers,
 // two CTAs per SM); same summation order as the 8-warp tile.
-template <int TN, bool Fat = false>
+// TM = 64: 64 x 64 tiles of 4 warps (32 x 32), three CTAs per SM -- the
+// shape cuBLAS picks for short-K batches (ncu at 256^3 x 64: 128 threads,
+// 126 registers, 65.5 KB, grid 1024): twice the tiles of 128 x 64, so the
+// small products of the first levels fill more waves.
+template <int TN, bool Fat = false, int TM = kBM>
 struct RefillCfg {
-  static constexpr int kWarpsT = Fat ? 4 : 4 * (TN / 32);
+  static constexpr int kWarpsT = Fat ? 4 : (TM / 32) * (TN / 32);
   static constexpr int kThr = kWarpsT * 32;
+  static constexpr int kStageA = TM * kBK * 8;
   static constexpr int kStageB = kBK * TN * 8;
   static constexpr int kStage = kStageA + kStageB;
-  static constexpr int kMinBlocks = TN == 64 ? 2 : 1;
+  static constexpr int kMinBlocks = TM == 64 ? 3 : (TN == 64 ? 2 : 1);
 };
-template <int kStages, int TN>
-constexpr int refill_smem() { return kStages * RefillCfg<TN>::kStage + 1024; }
+template <int kStages, int TN, int TM = kBM>
+constexpr int refill_smem() { return kStages * RefillCfg<TN, false, TM>::kStage + 1024; }
 
-template <int kStages, int TN, bool Fat = false>
-__global__ void __launch_bounds__(RefillCfg<TN, Fat>::kThr, RefillCfg<TN, Fat>::kMinBlocks)
+template <int kStages, int TN, bool Fat = false, int TM = kBM>
+__global__ void __launch_bounds__(RefillCfg<TN, Fat, TM>::kThr, RefillCfg<TN, Fat, TM>::kMinBlocks)
     gemm_tma_refill_kernel(const __grid_constant__ TmaLaunch L) {
   pdl_enter();
-  using Cfg = RefillCfg<TN, Fat>;
+  using Cfg = RefillCfg<TN, Fat, TM>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kStages];
@@ -229,12 +234,12 @@ __global__ void __launch_bounds__(RefillCfg<TN, Fat>::kThr, RefillCfg<TN, Fat>::
       ahead -= KT;
       tile += gridDim.x;
       if (tile >= L.total_tiles) return;
-      tc = k1_locate<kBM, TN>(L.d, L.count, tile);
+      tc = k1_locate<TM, TN>(L.d, L.count, tile);
       KT = (L.d[tc.desc].K + kBK - 1) / kBK;
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before async writes
     uint8_t* sa = smem + stage * Cfg::kStage;
-    uint8_t* sb = sa + kStageA;
+    uint8_t* sb = sa + Cfg::kStageA;
     mbar_expect_tx(&full[stage], Cfg::kStage);
     tma_load_3d(sa, &L.ta[tc.desc], &full[stage], ahead * kBK, tc.m0, tc.bz);
 #pragma unroll
@@ -242,14 +247,14 @@ __global__ void __launch_bounds__(RefillCfg<TN, Fat>::kThr, RefillCfg<TN, Fat>::
       tma_load_3d(sb + j * kBoxBBytes, &L.tb[tc.desc], &full[stage], tc.n0 + 16 * j, ahead * kBK, tc.bz);
   };
   if (tid == 0 && (int)blockIdx.x < L.total_tiles) {
-    const K1Tile t0 = k1_locate<kBM, TN>(L.d, L.count, blockIdx.x);
+    const K1Tile t0 = k1_locate<TM, TN>(L.d, L.count, blockIdx.x);
     const int KT0 = (L.d[t0.desc].K + kBK - 1) / kBK;
     for (int s = 0; s < kStages; ++s) fill(s, blockIdx.x, t0, KT0, s);
   }
 
   unsigned cons_it = 0;
   for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
-    const K1Tile tc = k1_locate<kBM, TN>(L.d, L.count, tile);
+    const K1Tile tc = k1_locate<TM, TN>(L.d, L.count, tile);
     const GemmDesc& d = L.d[tc.desc];
     const int KT = (d.K + kBK - 1) / kBK;
     constexpr int H = Fat ? 2 : 1;  // 32-row halves of the warp tile
@@ -265,9 +270,9 @@ __global__ void __launch_bounds__(RefillCfg<TN, Fat>::kThr, RefillCfg<TN, Fat>::
       const int stage = cons_it % kStages;
       mbar_wait(&full[stage], (cons_it / kStages) & 1);
       if constexpr (Fat) {
-        k1_compute_64x32<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
+        k1_compute_64x32<Cfg::kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc);
       } else {
-        k1_compute<kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc[0]);
+        k1_compute<Cfg::kStageA>(smem + stage * Cfg::kStage, f, wm, wn, fr, acc[0]);
       }
       __syncwarp();
       if (lane == 0 && release_stage(&released[stage], Cfg::kWarpsT)) {
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(RefillCfg<TN, Fat>::kThr, RefillCfg<TN, Fat>::
     }
 
 #pragma unroll
-    for (int h = 0; h < H; ++h) k1_epilogue<kBM, TN>(d, tc.bz, tc.m0, tc.n0, H * wm + h, wn, fr, fc, acc[h]);
+    for (int h = 0; h < H; ++h) k1_epilogue<TM, TN>(d, tc.bz, tc.m0, tc.n0, H * wm + h, wn, fr, fc, acc[h]);
   }
 }
 
@@ -547,6 +552,10 @@ cudaError_t tma_init() {
                                refill_smem<4, 64>());
     if (e == cudaSuccess) e = set_carveout(gemm_tma_refill_kernel<4, 64, true>);
     if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_tma_refill_kernel<4, 64, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               refill_smem<4, 64, 64>());
+    if (e == cudaSuccess) e = set_carveout(gemm_tma_refill_kernel<4, 64, false, 64>);
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_tma_kseg_kernel<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                refill_smem<4, 64>());
     if (e == cudaSuccess) e = set_carveout(gemm_tma_kseg_kernel<4, 64>);
@@ -659,6 +668,50 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
     const char* e = getenv("BI_GEMM_TN");
     return (e && atoi(e) == 128) ? 128 : 64;
   }();
+  // BI_GEMM_TM: 128 (default) or 64; BI_GEMM_TM=0 = 64 when every descriptor
+  // has K < BI_GEMM_TM64_K (512) and the 128 x 64 tiling has fewer than
+  // BI_GEMM_TM64_TILES (1200, ~4 waves of 296) tiles.  64 x 64 wins alone on
+  // short-K batches (256^3 x 64: 26.6 -> 28.0 TF/s; K3's 8-leaf K = 128 outer
+  // update 14.6 -> 17.1) but not inside the engine (cfg4 394.7 -> 395.4 ms,
+  // cfg2 26.9 -> 26.9; profiles/r02_k1_tiles.txt), so it stays opt-in.
+  static const int tm_env = [] {
+    const char* e = getenv("BI_GEMM_TM");
+    return e ? atoi(e) : 128;
+  }();
+  static const int tm64_k = [] {
+    const char* e = getenv("BI_GEMM_TM64_K");
+    return e ? atoi(e) : 512;
+  }();
+  static const int tm64_tiles = [] {
+    const char* e = getenv("BI_GEMM_TM64_TILES");
+    return e ? atoi(e) : 1200;
+  }();
+  int kmax = 0, t128 = 0;
+  for (int i = 0; i < count; ++i) {
+    const GemmDesc& d = L.d[i];
+    kmax = std::max(kmax, d.K);
+    if (d.M > 0 && d.N > 0 && d.batch > 0) t128 += ((d.M + kBM - 1) / kBM) * ((d.N + 63) / 64) * d.batch;
+  }
+  const int tm = tm_env == 64 || tm_env == 128 ? tm_env : (kmax < tm64_k && t128 < tm64_tiles ? 64 : 128);
+  if (refill && tn == 64 && tm == 64) {
+    int t = 0;
+    for (int i = 0; i < count; ++i) {
+      GemmDesc& d = L.d[i];
+      const bool empty = d.M <= 0 || d.N <= 0 || d.batch <= 0;
+      d.tiles_m = empty ? 0 : (d.M + 63) / 64;
+      d.tiles_n = empty ? 1 : (d.N + 63) / 64;
+      d.tile_begin = t;
+      t += empty ? 0 : d.tiles_m * d.tiles_n * d.batch;
+      const uint64_t batch = d.batch > 0 ? (uint64_t)d.batch : 1;
+      if (!encode_3d(&L.ta[i], d.A, (uint64_t)d.K, (uint64_t)d.M, batch, d.lda, d.sA, kBK, 64)) return false;
+    }
+    L.total_tiles = t;
+    const int cap3 = grid_cap > 0 ? 3 * grid_cap : 0;
+    const int grid3 = (cap3 > 0 && cap3 < t) ? cap3 : t;
+    *err = launch_kernel(gemm_tma_refill_kernel<4, 64, false, 64>, dim3(grid3),
+                         dim3(RefillCfg<64, false, 64>::kThr), (size_t)refill_smem<4, 64, 64>(), stream, 1u, L);
+    return true;
+  }
   if (refill && tn == 64) {
     // re-tile the descriptors for 128 x 64 tiles
     int t = 0;

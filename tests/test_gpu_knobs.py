@@ -55,6 +55,8 @@ KNOBS = [
     {"BI_GJ_FAST_SMALL": "1"},
     {"BI_GEMM_WARPS": "4"},
     {"BI_GEMM_WARPS": "8"},
+    {"BI_GEMM_TM": "64"},
+    {"BI_ENGINE_PDL": "1"},
 ]
 
 
@@ -91,19 +93,22 @@ print("ok")
 """
 
 
-def test_gemm_warp_tiles_bitwise(tmp_path):
-    """K1's 4-warp (64 x 32) and 8-warp (32 x 32) tiles sum every element in the
-    same order: bitwise equal outputs, including ragged shapes."""
+@pytest.mark.parametrize("variant", [{"BI_GEMM_WARPS": "4"}, {"BI_GEMM_TM": "64"}], ids=["warps4", "tm64"])
+def test_gemm_tile_variants_bitwise(tmp_path, variant):
+    """K1's tile variants -- 4 warps of 64 x 32, 64 x 64 CTA tiles -- sum every
+    element in the same order as the 8-warp 128 x 64 tile: bitwise equal
+    outputs, including ragged shapes."""
     res = {}
-    for w in ("4", "8"):
-        f = tmp_path / f"w{w}.npz"
-        env = dict(os.environ, BI_GEMM_WARPS=w)
+    base = {"BI_GEMM_WARPS": "8", "BI_GEMM_TM": "128"}
+    for w, knobs in (("v", variant), ("base", base)):
+        f = tmp_path / f"{w}.npz"
+        env = dict(os.environ, **knobs)
         r = subprocess.run([sys.executable, "-c", BITWISE_GEMM, str(ROOT), str(f)], env=env, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         res[w] = np.load(f)
-    for key in res["4"].files:
-        assert np.array_equal(res["4"][key], res["8"][key]), key
+    for key in res["v"].files:
+        assert np.array_equal(res["v"][key], res["base"][key]), key
 
 
 def test_fused_small_inverter_bitwise():
