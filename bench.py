@@ -451,7 +451,7 @@ def run_gpu_arm(args) -> None:
                 "api": "paper_2305_11103_b200.run_inversion(m, sizes=[256]*64), m a pageable NumPy array"},
         "roofline": {"bound": "tensor", "achieved": k1_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": k1_tflops / FP64_PEAK_TFLOPS, "traffic": _load_traffic(),
-                     "kernel": "gemm_tma_refill_kernel<4, 64> (K1 TMA feeder, engine GEMM ops)",
+                     "kernel": "gemm_tma_refill_kernel<4, 64, Fat> (K1 TMA feeder, engine GEMM ops; 4-warp 64x32 tiles for K >= 1024)",
                      "peak_source": FP64_PEAK_SOURCE,
                      "kernel_ms_per_step": gemm_ms, "kernel_flops_per_step": counters["gemm_flops"],
                      "share_of_step": gemm_ms / ms_step,
