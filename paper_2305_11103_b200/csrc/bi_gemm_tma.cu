@@ -727,7 +727,7 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
     const int cap2 = grid_cap > 0 ? 2 * grid_cap : 0;
     const int grid2 = (cap2 > 0 && cap2 < t) ? cap2 : t;
     // BI_GEMM_WARPS: 8 = 32 x 32 warp tiles, 4 = 64 x 32 (the cuBLAS shape),
-    // unset = 4 when every descriptor has K >= 1024.  Measured (tools/gemm_sweep.py,
+    // unset = 4 when every descriptor has K >= 1024 (see below).  Measured (tools/gemm_sweep.py,
     // profiles/r02_k1_fat_warps.txt): 4 warps win on long k loops (8192^3 34.50 ->
     // 35.41 TF/s, cuBLAS 35.48; 1024^3 x 16 33.93 -> 34.30) and lose on short ones
     // (512^3 x 32 32.8 -> 28.8; K3's K = 128 updates 22.5 -> 18.6), where fewer
@@ -736,9 +736,17 @@ bool launch_gemm_tma(const GemmDesc* h, int count, int grid_cap, cudaStream_t st
       const char* e = getenv("BI_GEMM_WARPS");
       return e ? atoi(e) : 0;
     }();
+    // ... and at least BI_GEMM_FAT_TILES (default 1184 = four waves of 2 x 148) tiles:
+    // with fewer, an SM often holds ONE 4-warp CTA (one warp per scheduler,
+    // which cannot keep the DMMA pipe busy: 34.0 vs 36.98 TF/s in the
+    // microbench) -- cfg3's 1000-wide via_d products lost 0.65 ms that way.
+    static const int fat_tiles = [] {
+      const char* e = getenv("BI_GEMM_FAT_TILES");
+      return e ? atoi(e) : 4 * 2 * 148;
+    }();
     int kmin = INT32_MAX;
     for (int i = 0; i < count; ++i) kmin = std::min(kmin, L.d[i].K);
-    const bool fat = warps_env == 4 || (warps_env != 8 && kmin >= 1024);
+    const bool fat = warps_env == 4 || (warps_env != 8 && kmin >= 1024 && t >= fat_tiles);
     if (fat)
       *err = launch_kernel(gemm_tma_refill_kernel<4, 64, true>, dim3(grid2), dim3(RefillCfg<64, true>::kThr),
                            (size_t)refill_smem<4, 64>(), stream, 1u, L);
