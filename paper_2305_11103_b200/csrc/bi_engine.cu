@@ -265,7 +265,7 @@ struct bi_engine {
   cudaStream_t copy_stream = nullptr;       // host->device input copies
   cudaStream_t d2h_stream[kMaxLanes] = {};  // per-lane read-back (page-locked output)
   cudaEvent_t ev_d2h_a[kMaxLanes] = {}, ev_d2h_b[kMaxLanes] = {};
-  static constexpr int kOutChunks = 4;  // row chunks of the last top-level pass, each read back at once
+  static constexpr int kOutChunks = 16;  // max row chunks of the last top-level pass, each read back at once
   cudaEvent_t ev_chunk[kMaxLanes][kOutChunks] = {};
   std::vector<cudaEvent_t> ev_h2d;          // per (matrix, level): that level's input blocks copied
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -1038,6 +1038,17 @@ extern "C" int bi_engine_bind(bi_engine* e, const double* m, int64_t ldm, int64_
 struct HostIO;
 static cudaError_t copy_top_quads(bi_engine* e, int lane, const HostIO* io, bool diag, cudaStream_t st);
 
+// BI_OUT_CHUNKS (default 8, max 16): row chunks of the last top-level pass, each read
+// back as soon as written (cfg4 run_inversion(m): 4 -> 408.4 / 407.4 ms, 8 -> 404.9 / 405.2, 16 -> 407.8)
+static int out_chunks() {
+  static const int c = [] {
+    const char* v = getenv("BI_OUT_CHUNKS");
+    const int x = v ? atoi(v) : 8;
+    return x < 1 ? 1 : (x > bi_engine::kOutChunks ? bi_engine::kOutChunks : x);
+  }();
+  return c;
+}
+
 static cudaError_t pass_in_chunks(bi_engine* e, int lane, const GemmLaunchRec& L, const HostIO* io,
                                   cudaStream_t s);
 
@@ -1161,7 +1172,7 @@ struct HostIO {
 static cudaError_t pass_in_chunks(bi_engine* e, int lane, const GemmLaunchRec& L, const HostIO* io,
                                   cudaStream_t s) {
   cudaError_t err = cudaSuccess;
-  const int C = bi_engine::kOutChunks;
+  const int C = out_chunks();
   for (int c = 0; c < C && err == cudaSuccess; ++c) {
     GemmDesc d[kGemmInline];
     int nd = 0;
