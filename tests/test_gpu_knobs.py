@@ -57,6 +57,8 @@ KNOBS = [
     {"BI_GEMM_WARPS": "8"},
     {"BI_GEMM_TM": "64"},
     {"BI_ENGINE_PDL": "1"},
+    {"BI_GJ_SUBLA": "1"},
+    {"BI_GJ_SUBLA": "1", "BI_GJ_FAST_SMALL": "1"},
 ]
 
 
@@ -111,10 +113,12 @@ def test_gemm_tile_variants_bitwise(tmp_path, variant):
         assert np.array_equal(res["v"][key], res["base"][key]), key
 
 
-def test_fused_small_inverter_bitwise():
-    """BI_GJ_FUSED=1 (one cluster launch per batch of blocks <= 512) is bitwise
-    the multi-launch chain, on dominant, random, permuted, singular, ragged and
-    tied blocks (tools/k3_fast_check.py)."""
-    r = subprocess.run([sys.executable, str(ROOT / "tools" / "k3_fast_check.py"), "BI_GJ_FUSED"], capture_output=True,
+@pytest.mark.parametrize("knob", ["BI_GJ_FUSED", "BI_GJ_SUBLA"])
+def test_k3_variants_bitwise(knob):
+    """BI_GJ_FUSED=1 (one cluster launch per batch of blocks <= 512) and
+    BI_GJ_SUBLA=1 (sub-panel lookahead) are bitwise the multi-launch chain, on
+    dominant, random, permuted, singular, ragged and tied blocks
+    (tools/k3_fast_check.py)."""
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "k3_fast_check.py"), knob], capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0 and "ALL BITWISE EQUAL" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
