@@ -60,9 +60,12 @@ if __name__ == "__main__":
     import tempfile
 
     knob = sys.argv[1] if len(sys.argv) > 1 else "BI_GJ_FAST"
-    print(f"{knob}=0 vs {knob}=1")
+    on = "1"
+    if "=" in knob:  # KNOB=VALUE: compare VALUE against 0
+        knob, on = knob.split("=", 1)
+    print(f"{knob}=0 vs {knob}={on}")
     outs = {}
-    for mode in ("0", "1"):
+    for mode in ("0", on):
         d = tempfile.mkdtemp()
         env = dict(os.environ, **{knob: mode})
         subprocess.run([sys.executable, __file__, d], env=env, check=True)
@@ -70,9 +73,9 @@ if __name__ == "__main__":
     ok = True
     for ci, (kind, cnt, n) in enumerate(CASES):
         a = np.load(os.path.join(outs["0"], f"c{ci}_x.npy"))
-        b = np.load(os.path.join(outs["1"], f"c{ci}_x.npy"))
+        b = np.load(os.path.join(outs[on], f"c{ci}_x.npy"))
         ia = np.load(os.path.join(outs["0"], f"c{ci}_i.npy"))
-        ib = np.load(os.path.join(outs["1"], f"c{ci}_i.npy"))
+        ib = np.load(os.path.join(outs[on], f"c{ci}_i.npy"))
         same = np.array_equal(a, b, equal_nan=True) and np.array_equal(ia, ib)
         ok &= same
         print(f"{kind:5s} {cnt:3d} x {n:5d}: bitwise {'equal' if same else 'DIFFERENT'}  info {ia.tolist()[:4]}")

@@ -180,6 +180,162 @@ __global__ void phase_a_2d(const double* in, double* out, long long* cyc, int re
   if (t == 0) cyc[blockIdx.x] = total / reps + bad;
 }
 
+// V6: lockstep column loop of the single-CTA panel (256 threads, one row each):
+// owner publishes row c, one barrier, every row updates.  MODE bit 1: skip rcp,
+// bit 2: skip the 30 row FMAs, bit 4: skip the objection check.
+template <int MODE>
+__global__ void lockstep(const double* in, double* out, long long* cyc, int reps) {
+  __shared__ __align__(16) double s_lrow[2][NB + 2];
+  const int t = threadIdx.x;
+  const double* src = in + (size_t)blockIdx.x * 256 * NB;
+  double P[NB];
+  long long total = 0;
+  int objection = 0;
+  for (int rep = 0; rep < reps; ++rep) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) P[k] = src[t * NB + k];
+    double rc = 1.0 / P[0];
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int c = 0; c < NB; ++c) {
+      const int buf = c & 1;
+      if (MODE & 32) {  // predicated stores, no branch
+        const unsigned base = (unsigned)__cvta_generic_to_shared(s_lrow[buf]);
+        const bool me = t == c;
+#pragma unroll
+        for (int k = 0; k < NB / 2; ++k) st_pred_v2(base + 16 * k, P[2 * k], P[2 * k + 1], me);
+        st_pred_f64(base + 8 * NB, rc, me);
+      } else if (t == c && !(MODE & 16)) {
+        double2* dst = reinterpret_cast<double2*>(s_lrow[buf]);
+#pragma unroll
+        for (int k = 0; k < NB / 2; ++k) dst[k] = make_double2(P[2 * k], P[2 * k + 1]);
+        s_lrow[buf][NB] = rc;
+      }
+      __syncthreads();
+      double prr[NB];
+      if (MODE & 8) {
+        const double v0 = s_lrow[buf][c & 7];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) prr[k] = v0 + k;
+      } else {
+#pragma unroll
+        for (int k = 0; k < NB / 2; ++k) {
+          const double2 v = reinterpret_cast<const double2*>(s_lrow[buf])[k];
+          prr[2 * k] = v.x;
+          prr[2 * k + 1] = v.y;
+        }
+      }
+      const double inv = s_lrow[buf][NB];
+      if (!(MODE & 4)) {
+        if (t > c && fabs(P[0]) > fabs(prr[0])) objection = 1;
+      }
+      const bool isp = t == c;
+      const double fi = isp ? 1.0 - inv : P[0] * inv;
+      const double ti = isp ? inv : -fi;
+      P[0] = fma(-fi, prr[1], P[1]);
+      if (!(MODE & 1)) rc = fast_rcp(P[0]);
+      else rc = P[0];
+      if (!(MODE & 2)) {
+#pragma unroll
+        for (int k = 1; k < NB - 1; ++k) P[k] = fma(-fi, prr[k + 1], P[k + 1]);
+      }
+      P[NB - 1] = ti;
+    }
+    const long long t1 = clock64();
+    total += t1 - t0;
+  }
+#pragma unroll
+  for (int k = 0; k < NB; ++k) out[(size_t)blockIdx.x * 256 * NB + t * NB + k] = P[k];
+  if (t == 0) cyc[blockIdx.x] = total / reps + objection;
+}
+
+// V7: lockstep with 8 x 4 blocks per thread (256 threads: i = t / 8 row block,
+// j = t % 8 column block): per step the column-c owners publish their 8
+// values, the row-c owners their 4, one barrier, every thread reads 8 + 4 + 1.
+template <int STATIC>
+__global__ void __launch_bounds__(256, 1) lockstep2d(const double* in, double* out, long long* cyc, int reps) {
+  __shared__ __align__(16) double s_col[2][256], s_row[2][NB + 2];
+  const int t = threadIdx.x, bi = t >> 3, bj = t & 7;
+  const double* src = in + (size_t)blockIdx.x * 256 * NB;
+  double w[8][4];
+  long long total = 0;
+  int objection = 0;
+  for (int rep = 0; rep < reps; ++rep) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) w[a][b] = src[(bi * 8 + a) * NB + bj * 4 + b];
+    if (t == 0) s_row[0][NB] = 1.0 / w[0][0];
+    __syncthreads();
+    const long long t0 = clock64();
+#pragma unroll 1
+    for (int c = 0; c < NB; ++c) {
+      const int buf = c & 1;
+      // publish column c (owners: bj == c / 4) and row c (owners: bi == c / 8)
+      if (bj == (c >> 2)) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          double v = w[a][0];
+          if (!STATIC) {
+#pragma unroll
+            for (int b = 1; b < 4; ++b) v = (c & 3) == b ? w[a][b] : v;
+          }
+          s_col[buf][bi * 8 + a] = v;
+        }
+      }
+      if (bi == (c >> 3)) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          double v = w[0][b];
+          if (!STATIC) {
+#pragma unroll
+            for (int a = 1; a < 8; ++a) v = (c & 7) == a ? w[a][b] : v;
+          }
+          s_row[buf][bj * 4 + b] = v;
+        }
+      }
+      __syncthreads();
+      const double inv = s_row[buf][NB];
+      double x[8], pr[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) x[a] = s_col[buf][bi * 8 + a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) pr[b] = s_row[buf][bj * 4 + b];
+      const double pc = s_row[buf][c];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const int r = bi * 8 + a;
+        if (r > c && fabs(x[a]) > fabs(pc)) objection = 1;
+        const bool isp = r == c;
+        const double fi = isp ? 1.0 - inv : x[a] * inv;
+        const double ti = isp ? inv : -fi;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) w[a][b] = (!STATIC && bj * 4 + b == c) ? ti : fma(-fi, pr[b], w[a][b]);
+      }
+      // the next pivot's reciprocal
+      if (bi == ((c + 1) >> 3) && bj == ((c + 1) >> 2) && c + 1 < NB) {
+        double v = w[0][0];
+        if (!STATIC) {
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (bi * 8 + a == c + 1 && bj * 4 + b == c + 1) v = w[a][b];
+        }
+        s_row[buf ^ 1][NB] = fast_rcp(v);
+      }
+    }
+    const long long t1 = clock64();
+    total += t1 - t0;
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) out[(size_t)blockIdx.x * 256 * NB + (bi * 8 + a) * NB + bj * 4 + b] = w[a][b];
+  if (t == 0) cyc[blockIdx.x] = total / reps + objection;
+}
+
 int main() {
   const int blocks = 64, reps = 20;
   std::vector<double> h((size_t)blocks * NB * NB);
@@ -218,6 +374,47 @@ int main() {
   printf("  V2 bitwise %s\n", memcmp(ref.data(), got.data(), ref.size() * 8) ? "DIFFER" : "equal");
   run(phase_a_2d, "V5 CTA-wide 2D (256 thr)", got);
   printf("  V5 bitwise %s\n", memcmp(ref.data(), got.data(), ref.size() * 8) ? "DIFFER" : "equal");
+  {
+    const int lb = 64;
+    std::vector<double> h2((size_t)lb * 256 * NB);
+    for (size_t i = 0; i < h2.size(); ++i) h2[i] = ((i * 2654435761u) % 1000) / 16000.0;
+    for (int b = 0; b < lb; ++b)
+      for (int i = 0; i < NB; ++i) h2[(size_t)b * 256 * NB + i * NB + i] += 4.0;
+    double *d2, *o2;
+    cudaMalloc(&d2, h2.size() * 8);
+    cudaMalloc(&o2, h2.size() * 8);
+    cudaMemcpy(d2, h2.data(), h2.size() * 8, cudaMemcpyHostToDevice);
+    long long* c2;
+    cudaMalloc(&c2, lb * 8);
+    auto runl = [&](auto kern, const char* name) {
+      kern<<<lb, 256>>>(d2, o2, c2, reps);
+      cudaDeviceSynchronize();
+      std::vector<long long> cc(lb);
+      cudaMemcpy(cc.data(), c2, lb * 8, cudaMemcpyDeviceToHost);
+      long long sum = 0;
+      for (auto v : cc) sum += v;
+      printf("%-34s %6lld cyc / 32 steps = %.1f cyc/step\n", name, sum / lb, (double)sum / lb / 32);
+    };
+    runl(lockstep<0>, "V6 lockstep 256 thr (full)");
+    runl(lockstep<1>, "V6 lockstep, no rcp");
+    runl(lockstep<2>, "V6 lockstep, no row FMAs");
+    runl(lockstep<4>, "V6 lockstep, no objection check");
+    runl(lockstep<7>, "V6 lockstep, barrier+bcast only");
+    runl(lockstep<15>, "V6 barrier + 1-value bcast only");
+    runl(lockstep<23>, "V6 barrier + bcast, no owner STS");
+    runl(lockstep<32>, "V6 lockstep full, predicated STS");
+    runl(lockstep<39>, "V6 barrier+bcast, predicated STS");
+    runl(lockstep2d<0>, "V7 lockstep 8x4 blocks");
+    runl(lockstep2d<1>, "V7 static publish (timing only)");
+    {  // bitwise: V6 full vs V7
+      std::vector<double> a6(h2.size()), a7(h2.size());
+      lockstep<0><<<lb, 256>>>(d2, o2, c2, 1);
+      cudaMemcpy(a6.data(), o2, a6.size() * 8, cudaMemcpyDeviceToHost);
+      lockstep2d<0><<<lb, 256>>>(d2, o2, c2, 1);
+      cudaMemcpy(a7.data(), o2, a7.size() * 8, cudaMemcpyDeviceToHost);
+      printf("  V7 vs V6 bitwise %s\n", memcmp(a6.data(), a7.data(), a6.size() * 8) ? "DIFFER" : "equal");
+    }
+  }
   run(phase_a<3>, "V3 shfl, no rcp (timing)", got);
   run(phase_a<4>, "V4 shfl, no row FMAs (timing)", got);
   chains<<<1, 32>>>(dc);
