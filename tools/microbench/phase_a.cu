@@ -336,6 +336,71 @@ __global__ void __launch_bounds__(256, 1) lockstep2d(const double* in, double* o
   if (t == 0) cyc[blockIdx.x] = total / reps + objection;
 }
 
+// V8: lockstep with TWO threads per row (512 threads, lanes 2i / 2i+1 = row
+// halves): register rotation over the 32 columns split 16 / 16, the boundary
+// value and the multiplier exchanged by one shuffle each; the owner pair
+// publishes 8 + 8 values, readers load only their half.
+constexpr int H = NB / 2;
+__global__ void __launch_bounds__(512, 1) lockstep2(const double* in, double* out, long long* cyc, int reps) {
+  __shared__ __align__(16) double s_lrow[2][NB + 2];
+  const int t = threadIdx.x, row = t >> 1, h = t & 1;
+  const double* src = in + (size_t)blockIdx.x * 256 * NB;
+  double P[H];
+  long long total = 0;
+  int objection = 0;
+  for (int rep = 0; rep < reps; ++rep) {
+#pragma unroll
+    for (int k = 0; k < H; ++k) P[k] = src[row * NB + h * H + k];
+    double rc = h == 0 ? fast_rcp(P[0]) : 0.0;
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int c = 0; c < NB; ++c) {
+      const int buf = c & 1;
+      if (row == c) {  // the owner pair publishes its halves (rotated row: P of h=0 = cols c.., h=1 = rest)
+        double2* dst = reinterpret_cast<double2*>(s_lrow[buf] + h * H);
+#pragma unroll
+        for (int k = 0; k < H / 2; ++k) dst[k] = make_double2(P[2 * k], P[2 * k + 1]);
+        if (h == 0) s_lrow[buf][NB] = rc;
+      }
+      __syncthreads();
+      // reader: needs prr[k + 1] for its registers k: h = 0 -> pr[1 .. 16], h = 1 -> pr[17 .. 31] (+ none)
+      double prr[H + 1];
+#pragma unroll
+      for (int k = 0; k < H / 2; ++k) {
+        const double2 v = reinterpret_cast<const double2*>(s_lrow[buf] + h * H)[k];
+        prr[2 * k] = v.x;
+        prr[2 * k + 1] = v.y;
+      }
+      prr[H] = h == 0 ? s_lrow[buf][H] : 0.0;
+      const double inv = s_lrow[buf][NB];
+      // multiplier from the h = 0 thread (it holds the current column), boundary from h = 1
+      const double x = __shfl_sync(0xffffffffu, P[0], (threadIdx.x & 31) & ~1);
+      const double nb0 = __shfl_down_sync(0xffffffffu, P[0], 1);  // h=0 receives h=1's old P[0]
+      if (h == 0 && row > c && fabs(x) > fabs(prr[0])) objection = 1;
+      const bool isp = row == c;
+      const double fi = isp ? 1.0 - inv : x * inv;
+      const double ti = isp ? inv : -fi;
+      if (h == 0) {
+        P[0] = fma(-fi, prr[1], P[1]);
+        rc = fast_rcp(P[0]);
+#pragma unroll
+        for (int k = 1; k < H - 1; ++k) P[k] = fma(-fi, prr[k + 1], P[k + 1]);
+        P[H - 1] = fma(-fi, prr[H], nb0);
+      } else {
+#pragma unroll
+        for (int k = 0; k < H - 1; ++k) P[k] = fma(-fi, prr[k + 1], P[k + 1]);
+        P[H - 1] = ti;
+      }
+    }
+    const long long t1 = clock64();
+    total += t1 - t0;
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < H; ++k) out[(size_t)blockIdx.x * 256 * NB + row * NB + h * H + k] = P[k];
+  if (t == 0) cyc[blockIdx.x] = total / reps + objection;
+}
+
 int main() {
   const int blocks = 64, reps = 20;
   std::vector<double> h((size_t)blocks * NB * NB);
@@ -405,6 +470,22 @@ int main() {
     runl(lockstep<32>, "V6 lockstep full, predicated STS");
     runl(lockstep<39>, "V6 barrier+bcast, predicated STS");
     runl(lockstep2d<0>, "V7 lockstep 8x4 blocks");
+    {
+      lockstep2<<<lb, 512>>>(d2, o2, c2, reps);
+      cudaDeviceSynchronize();
+      std::vector<long long> cc(lb);
+      cudaMemcpy(cc.data(), c2, lb * 8, cudaMemcpyDeviceToHost);
+      long long sum = 0;
+      for (auto v : cc) sum += v;
+      printf("%-34s %6lld cyc / 32 steps = %.1f cyc/step\n", "V8 lockstep 2 thr/row (512 thr)", sum / lb, (double)sum / lb / 32);
+      std::vector<double> a6(h2.size()), a8(h2.size());
+      lockstep<0><<<lb, 256>>>(d2, o2, c2, 1);
+      cudaMemcpy(a6.data(), o2, a6.size() * 8, cudaMemcpyDeviceToHost);
+      lockstep2<<<lb, 512>>>(d2, o2, c2, 1);
+      cudaMemcpy(a8.data(), o2, a8.size() * 8, cudaMemcpyDeviceToHost);
+      printf("  V8 vs V6 bitwise %s (%s)\n", memcmp(a6.data(), a8.data(), a6.size() * 8) ? "DIFFER" : "equal",
+             cudaGetErrorString(cudaGetLastError()));
+    }
     runl(lockstep2d<1>, "V7 static publish (timing only)");
     {  // bitwise: V6 full vs V7
       std::vector<double> a6(h2.size()), a7(h2.size());
