@@ -114,6 +114,12 @@ def stress(reps: int = 200) -> None:
     a, b, c = (dev(g.standard_normal(s)) for s in ((1024, 768), (768, 1280), (1024, 1280)))
     d = _lib.empty_matrix(1024, 1280)
     check("k1_tma_refill", lambda: (device_gemm(a, b, d, c=c), d.clone())[1])
+    af, bf = dev(g.standard_normal((2560, 1024))), dev(g.standard_normal((1024, 4096)))
+    df = _lib.empty_matrix(2560, 4096)
+    check("k1_fat_4warp", lambda: (device_gemm(af, bf, df), df.clone())[1])  # K >= 1024, 1280 tiles
+    x64 = dev(g.standard_normal((64, 256, 256)) / 16 + 4 * np.eye(256))
+    o64 = _lib.empty_matrix(256, 256, batch=64)
+    check("k3_64x256", lambda: (device_inverse(x64, o64), o64.clone())[1])
     segs = [dev(g.standard_normal((512, w))) for w in (128, 256, 64)]
     bb = dev(g.standard_normal((448, 384)))
     dk = _lib.empty_matrix(512, 384)
