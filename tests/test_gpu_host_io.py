@@ -177,3 +177,40 @@ def test_ring_path_for_buffers_above_the_staging_limit(tmp_path):
     script.write_text(_RING_SCRIPT)
     r = subprocess.run([sys.executable, str(script), str(root)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ring ok" in r.stdout, r.stdout + r.stderr
+
+
+_CHUNKS_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2305_11103_b200 as bi
+from conftest import well_conditioned
+for sizes, batch in (([64] * 8, 1), ([37, 29, 51, 16, 44, 23, 60, 8], 2), ([128] * 16, 1)):
+    n = sum(sizes)
+    ms = np.stack([well_conditioned(n, 120 + b) for b in range(batch)])
+    eng = bi.DeviceEngine(sizes, batch=batch)
+    eng.load(ms); eng.run(); eng.check()
+    ref = eng.Minv[:, :, :n].cpu().numpy()
+    pin_in = torch.from_numpy(ms).pin_memory().numpy()
+    pin_out = torch.full(ms.shape, float("nan"), dtype=torch.float64, pin_memory=True).numpy()
+    eng.run_host(pin_in, pin_out); eng.check()
+    assert np.array_equal(pin_out, ref), sizes
+print("chunks ok")
+"""
+
+
+@pytest.mark.parametrize("chunks", ["1", "3", "16"])
+def test_last_pass_read_back_chunks(tmp_path, chunks):
+    """The last top-level pass runs in BI_OUT_CHUNKS row chunks, each read back
+    as soon as it is written (page-locked output): any chunk count gives the
+    device-resident inverse bitwise, ragged partitions and batches included."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, BI_OUT_CHUNKS=chunks, PYTHONPATH=os.pathsep.join([str(root), str(root / "tests")]))
+    script = tmp_path / "chunks.py"
+    script.write_text(_CHUNKS_SCRIPT)
+    r = subprocess.run([sys.executable, str(script), str(root)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "chunks ok" in r.stdout, r.stdout + r.stderr
