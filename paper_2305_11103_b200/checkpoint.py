@@ -169,6 +169,75 @@ def checkpoint_save(directory, sizes, minv: np.ndarray, tsets: dict, completed_s
     (root / "meta.json").write_text(json.dumps(meta, indent=1))
 
 
+class CheckpointWriter:
+    """checkpoint_save for the step loop of a checkpointed run: the same files
+    and meta.json byte for byte, but a block whose values did not change since
+    this writer's previous save is neither rewritten nor rehashed (each step
+    touches only its own output blocks and new provisional entries), the
+    remaining blocks are serialised, hashed and written on a thread pool
+    (hashlib and file writes release the GIL), and the state hash comes from
+    the hashes of the bytes just written instead of reading every file back.
+    Files in the directory that this writer did not produce are hashed from
+    disk, so the state hash is _state_hash's in every case."""
+
+    def __init__(self, threads: int | None = None):
+        self._cache: dict[str, tuple[str, np.ndarray]] = {}  # relpath -> (sha256 hex of the file, values)
+        self._threads = threads or min(16, os.cpu_count() or 1)
+
+    def save(self, directory, sizes, minv: np.ndarray, tsets: dict, completed_step: int, input_hash: str) -> None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        root = Path(directory)
+        root.mkdir(parents=True, exist_ok=True)
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
+        nb = len(sizes)
+        blocks = []  # (relpath, array)
+        (root / "minv").mkdir(exist_ok=True)
+        for i in range(nb):
+            for j in range(nb):
+                blocks.append((f"minv/B_{i}_{j}.blk", minv[off[i]:off[i + 1], off[j]:off[j + 1]]))
+        for level, entries in tsets.items():
+            (root / "tset" / str(level)).mkdir(parents=True, exist_ok=True)
+            for (kind, idx), values in entries.items():
+                blocks.append((f"tset/{level}/{kind}_{idx}.blk", values))
+
+        cache = self._cache
+
+        def write(item):  # compare, and only if changed serialise, hash, write (numpy / hashlib / IO drop the GIL)
+            rel, values = item
+            hit = cache.get(rel)
+            if hit is not None and hit[1].shape == values.shape and np.array_equal(hit[1], values) \
+                    and (root / rel).exists():
+                return None
+            buf = matrix_to_bytes(values)
+            (root / rel).write_bytes(buf)
+            return rel, hashlib.sha256(buf).hexdigest(), np.array(values, dtype=np.float64, copy=True)
+
+        with ThreadPoolExecutor(self._threads) as pool:
+            for res in pool.map(write, blocks):
+                if res is not None:
+                    cache[res[0]] = (res[1], res[2])
+        h = hashlib.sha256()
+        h.update(f"stepid={completed_step}\n".encode())
+        for path in _blk_files(root):
+            rel = str(path.relative_to(root))
+            hit = self._cache.get(rel)
+            digest = hit[0] if hit is not None else hashlib.sha256(path.read_bytes()).hexdigest()
+            h.update(rel.encode())
+            h.update(b":")
+            h.update(digest.encode())
+            h.update(b"\n")
+        meta = {
+            "version": CHECKPOINT_VERSION,
+            "stepid": completed_step,
+            "blocksize": nb,
+            "sizes": list(int(x) for x in sizes),
+            "input_hash": input_hash,
+            "state_hash": h.hexdigest(),
+        }
+        (root / "meta.json").write_text(json.dumps(meta, indent=1))
+
+
 def load_state(directory, sizes):
     """(minv dense, {level: {(kind, idx): array}}) of a verified checkpoint."""
     root = Path(directory)

@@ -394,17 +394,31 @@ class DeviceEngine:
         ``stepid`` -- the state the reference checkpoints (storage.py:292-328)."""
         if self.schedule != "eq7":
             raise ValueError("step-boundary state exists for the Eq. 7 schedule only")
-        minv = self.Minv[matrix, :, : self.n].cpu().numpy()
+        t = _lib.torch()
+
+        def to_host(dev):  # DMA into page-locked memory (torch's caching host allocator), one sync at the end
+            host = t.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
+            host.copy_(dev, non_blocking=True)
+            return host
+
+        minv_h = to_host(self.Minv[matrix, :, : self.n])
+        squares = {}
+        for level in self.tset_levels_after(stepid):
+            for g in range(len(self.sizes) >> level):
+                squares[(level, g)] = to_host(self.tset_square(level, g, matrix))
+        t.cuda.current_stream().synchronize()
+        minv = minv_h.numpy()
         tsets = {}
         for level in self.tset_levels_after(stepid):
             entries = {}
             for g in range(len(self.sizes) >> level):
                 ha, hd = self._quad_spans(level, g)
-                sq = self.tset_square(level, g, matrix).cpu().numpy()
-                entries[("L", g)] = np.ascontiguousarray(sq[ha:, :ha])
-                entries[("R", g)] = np.ascontiguousarray(sq[:ha, ha:])
-                entries[("S", 2 * g)] = np.ascontiguousarray(sq[:ha, :ha])
-                entries[("S", 2 * g + 1)] = np.ascontiguousarray(sq[ha:, ha:])
+                sq = squares[(level, g)].numpy()
+                # views into the page-locked copy (serialised contiguously when written)
+                entries[("L", g)] = sq[ha:, :ha]
+                entries[("R", g)] = sq[:ha, ha:]
+                entries[("S", 2 * g)] = sq[:ha, :ha]
+                entries[("S", 2 * g + 1)] = sq[ha:, ha:]
             tsets[level] = entries
         return minv, tsets
 
@@ -616,11 +630,12 @@ def _run_checkpointed(scheme, dense, directory, file_backed, stop_after_step, co
     elif file_backed:
         ckpt.clear_state(directory)
     last = n_steps if stop_after_step is None else min(n_steps, max(start, int(stop_after_step)))
+    writer = ckpt.CheckpointWriter()  # checkpoint_save's files, unchanged blocks not rewritten
     for stepid in range(start, last + 1):
         eng.run(stepid, stepid, use_graph=False)
         eng.check()
         minv, tsets = eng.snapshot(stepid)
-        ckpt.checkpoint_save(directory, sizes, minv, tsets, stepid, input_hash)
+        writer.save(directory, sizes, minv, tsets, stepid, input_hash)
     if counters is not None and start <= last:
         c = eng.counters(start, last)
         counters.multiplies += c["multiplies"]

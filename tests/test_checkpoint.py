@@ -99,3 +99,37 @@ def test_reader_returns_reference_state_and_checks_integrity(tmp_path):
 def test_missing_meta(tmp_path):
     with pytest.raises(CheckpointCorrupt):
         ckpt.checkpoint_load(tmp_path)  # test_storage.py:118-120
+
+
+def _tree(root: Path) -> dict:
+    return {str(p.relative_to(root)): p.read_bytes() for p in sorted(root.rglob("*")) if p.is_file()}
+
+
+def test_incremental_writer_matches_checkpoint_save(tmp_path):
+    """CheckpointWriter (the checkpointed run's writer: unchanged blocks are
+    neither rewritten nor rehashed, the rest written on a thread pool) leaves
+    the directory byte for byte as checkpoint_save does, step after step, and
+    hashes files it did not write (a stale block) from disk like _state_hash."""
+    sizes = [3, 5, 4, 4]
+    n = sum(sizes)
+    g = np.random.default_rng(9)
+    minv = np.zeros((n, n))
+    tsets: dict = {}
+    ref_dir, new_dir = tmp_path / "ref", tmp_path / "new"
+    new_dir.mkdir()
+    (new_dir / "tset").mkdir()
+    stale = np.arange(6.0).reshape(2, 3)
+    for d in (ref_dir, new_dir):  # a block file neither writer produces
+        (d / "tset").mkdir(parents=True, exist_ok=True)
+        ckpt.save_binary(stale, d / "tset" / "stale.blk")
+    writer = ckpt.CheckpointWriter(threads=3)
+    for step in range(1, 6):
+        i, j = g.integers(0, len(sizes), 2)  # this step touches one block of M_inv ...
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        minv[off[i]:off[i + 1], off[j]:off[j + 1]] = g.standard_normal((sizes[i], sizes[j]))
+        if step % 2 == 0:  # ... and every other step adds provisional entries
+            tsets.setdefault(1, {})[("L", step)] = g.standard_normal((4, 3))
+        ckpt.checkpoint_save(ref_dir, sizes, minv, tsets, step, "h")
+        writer.save(new_dir, sizes, minv, tsets, step, "h")
+        assert _tree(ref_dir) == _tree(new_dir), step
+    assert ckpt.checkpoint_load(new_dir)["stepid"] == 5
