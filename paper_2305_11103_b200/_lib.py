@@ -213,6 +213,55 @@ def to_device(a: np.ndarray):
     return d
 
 
+_copy_pool = None
+
+
+def _threaded_copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """np.copyto(dst, src) by row chunks on a persistent thread pool (numpy
+    drops the GIL in copies): pageable <-> page-locked staging at host-memory
+    speed instead of one core's."""
+    global _copy_pool
+    threads = min(16, os.cpu_count() or 1, max(1, src.nbytes >> 23))
+    if threads <= 1 or src.ndim != 2:
+        np.copyto(dst, src)
+        return
+    if _copy_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _copy_pool = ThreadPoolExecutor(min(16, os.cpu_count() or 1))
+    rows = src.shape[0]
+    bounds = [rows * i // threads for i in range(threads + 1)]
+    list(_copy_pool.map(lambda i: np.copyto(dst[bounds[i]:bounds[i + 1]], src[bounds[i]:bounds[i + 1]]),
+                        range(threads)))
+
+
+def upload(a: np.ndarray):
+    """to_device for large host matrices: threaded copy into page-locked
+    memory (torch's caching host allocator), then one DMA."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.nbytes < (16 << 20):
+        return to_device(a)
+    t = torch()
+    d = empty_matrix(a.shape[0], a.shape[1])
+    pin = t.empty(a.shape, dtype=t.float64, pin_memory=True)
+    _threaded_copy(pin.numpy(), a)
+    d.copy_(pin, non_blocking=True)  # the allocator holds `pin` until this copy has run
+    return d
+
+
+def download(d, out: np.ndarray) -> None:
+    """out[...] = d for large matrices: one DMA into page-locked memory, then
+    a threaded copy into the caller's array."""
+    t = torch()
+    if out.ndim != 2 or out.nbytes < (16 << 20) or out.dtype != np.float64:
+        out[...] = d.cpu().numpy()
+        return
+    pin = t.empty(tuple(out.shape), dtype=t.float64, pin_memory=True)
+    pin.copy_(d, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    _threaded_copy(out, pin.numpy())
+
+
 def workspace(nbytes: int):
     t = torch()
     return t.empty((max(int(nbytes), 256),), dtype=t.uint8, device=require_device())

@@ -423,6 +423,28 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
   // info slots: 0 = A, 1 = D, 2 = SchurA, 3 = SchurD, 4 = B, 5 = C, 6 = SchurB, 7 = SchurC
   char labels[8] = {'A', 'D', 'a', 'd', 'B', 'C', 'b', 'c'};
   int order[4] = {0, 1, 2, 3};
+  // A singular pivot block ends the formula at once (one sync after its
+  // inversion), so invert_with_fallback's failed attempts cost one block
+  // inversion instead of the whole formula (cfg3's via_a: ~2 ms, not ~17).
+  auto early_singular = [&](std::initializer_list<int> slots) -> int {
+    int h[8];
+    if (cudaMemcpyAsync(h, info, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return -1;
+    for (int slot : slots)
+      if (h[slot] != 0) {
+        if (fail_block) *fail_block = labels[slot];
+        set_error(std::string("singular pivot block ") + labels[slot]);
+        return 1;
+      }
+    return 0;
+  };
+#define BI_EARLY(...)                                          \
+  do {                                                         \
+    const int r_ = early_singular({__VA_ARGS__});              \
+    BI_REQUIRE(r_ >= 0, "bi_schur2x2: CUDA error reading info"); \
+    if (r_) return 1;                                          \
+  } while (0)
   // counter-diagonal layout (schur.py:92-101): rows split at p, columns at q = n - p
   const double* cA = m;                 // p x q
   const double* cB = m + q;             // p x p
@@ -435,6 +457,7 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
   if (pivot == 'B') {
     // schur.py:167-190, S_B = C - D B^-1 A
     BI_CUDA_TRY(inv1(p, cB, ldm, Pinv, p, scratch, info + 4, s));
+    BI_EARLY(4);
     BI_CUDA_TRY(gemm1(p, q, p, 1, Pinv, p, cA, ldm, nullptr, 0, Y, q, s));     // Y = -B^-1 A
     BI_CUDA_TRY(gemm1(q, p, p, 0, cD, ldm, Pinv, p, nullptr, 0, X, p, s));     // X = D B^-1
     BI_CUDA_TRY(gemm1(q, q, p, 0, cD, ldm, Y, q, cC, ldm, S, q, s));           // S_B = C + D Y
@@ -449,6 +472,7 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
   } else if (pivot == 'C') {
     // schur.py:193-216, S_C = B - A C^-1 D
     BI_CUDA_TRY(inv1(q, cC, ldm, Qinv, q, scratch, info + 5, s));
+    BI_EARLY(5);
     BI_CUDA_TRY(gemm1(q, p, q, 1, Qinv, q, cD, ldm, nullptr, 0, X, p, s));     // X = -C^-1 D
     BI_CUDA_TRY(gemm1(p, q, q, 0, cA, ldm, Qinv, q, nullptr, 0, Y, q, s));     // Y = A C^-1
     BI_CUDA_TRY(gemm1(p, p, q, 0, cA, ldm, X, p, cB, ldm, S, p, s));           // S_C = B + A X
@@ -464,6 +488,7 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
     // schur.py:262-297 (combined counter-diagonal form)
     BI_CUDA_TRY(inv1(p, cB, ldm, Pinv, p, scratch, info + 4, s));
     BI_CUDA_TRY(inv1(q, cC, ldm, Qinv, q, scratch, info + 5, s));
+    BI_EARLY(4, 5);
     BI_CUDA_TRY(gemm1(p, q, p, 1, Pinv, p, cA, ldm, nullptr, 0, Y, q, s));     // Y = -B^-1 A
     BI_CUDA_TRY(gemm1(q, p, q, 1, Qinv, q, cD, ldm, nullptr, 0, X, p, s));     // X = -C^-1 D
     BI_CUDA_TRY(gemm1(q, q, p, 0, cD, ldm, Y, q, cC, ldm, S, q, s));           // S_B = C + D Y
@@ -479,6 +504,7 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
   } else if (pivot == 'A') {
     // schur.py:114-139
     BI_CUDA_TRY(inv1(p, A, ldm, Pinv, p, scratch, info + 0, s));
+    BI_EARLY(0);
     BI_CUDA_TRY(gemm1(p, q, p, 1, Pinv, p, B, ldm, nullptr, 0, Y, q, s));      // Y = -A^-1 B
     BI_CUDA_TRY(gemm1(q, p, p, 0, C, ldm, Pinv, p, nullptr, 0, X, p, s));      // X = C A^-1
     BI_CUDA_TRY(gemm1(q, q, p, 0, C, ldm, Y, q, D, ldm, S, q, s));             // S_A = D + C Y
@@ -491,6 +517,7 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
   } else if (pivot == 'D') {
     // schur.py:142-164
     BI_CUDA_TRY(inv1(q, D, ldm, Qinv, q, scratch, info + 1, s));
+    BI_EARLY(1);
     BI_CUDA_TRY(gemm1(q, p, q, 1, Qinv, q, C, ldm, nullptr, 0, X, p, s));      // X = -D^-1 C
     BI_CUDA_TRY(gemm1(p, q, q, 0, B, ldm, Qinv, q, nullptr, 0, Y, q, s));      // Y = B D^-1
     BI_CUDA_TRY(gemm1(p, p, q, 0, B, ldm, X, p, A, ldm, S, p, s));             // S_D = A + B X
@@ -506,6 +533,7 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
     // schur.py:219-259 (Eq. 7); S_D first, then S_A
     BI_CUDA_TRY(inv1(p, A, ldm, Pinv, p, scratch, info + 0, s));
     BI_CUDA_TRY(inv1(q, D, ldm, Qinv, q, scratch, info + 1, s));
+    BI_EARLY(0, 1);
     BI_CUDA_TRY(gemm1(p, q, p, 1, Pinv, p, B, ldm, nullptr, 0, Y, q, s));      // Y = -A^-1 B
     BI_CUDA_TRY(gemm1(q, p, q, 1, Qinv, q, C, ldm, nullptr, 0, X, p, s));      // X = -D^-1 C
     BI_CUDA_TRY(gemm1(p, p, q, 0, B, ldm, X, p, A, ldm, S, p, s));             // S_D = A + B X
@@ -517,6 +545,7 @@ extern "C" int bi_schur2x2(int pivot, int64_t n, int64_t p, const double* m, int
     order[2] = 3;
     order[3] = 2;
   }
+#undef BI_EARLY
   int h[8];
   BI_CUDA_TRY(cudaMemcpyAsync(h, info, sizeof(h), cudaMemcpyDeviceToHost, s));
   BI_CUDA_TRY(cudaStreamSynchronize(s));
