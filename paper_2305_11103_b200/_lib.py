@@ -200,16 +200,28 @@ def empty_matrix(rows: int, cols: int, batch: int | None = None):
     return t.empty((batch, rows, ld), dtype=t.float64, device=dev)[:, :, :cols]
 
 
+_STAGE_MIN = 16 << 20  # bytes above which host <-> device copies go through page-locked staging
+
+
 def to_device(a: np.ndarray):
+    """Host float64 matrix (or batch) -> padded device storage.  Large arrays
+    are copied into page-locked memory by several threads, then DMA'd (a
+    pageable copy runs at one core's speed and blocks the DMA)."""
     a = np.asarray(a, dtype=np.float64)
     if a.ndim == 2:
         d = empty_matrix(a.shape[0], a.shape[1])
     else:
         d = empty_matrix(a.shape[1], a.shape[2], batch=a.shape[0])
+    t = torch()
+    if a.nbytes >= _STAGE_MIN:
+        pin = t.empty(a.shape, dtype=t.float64, pin_memory=True)
+        _threaded_copy(pin.numpy().reshape(-1, a.shape[-1]), a.reshape(-1, a.shape[-1]))
+        d.copy_(pin, non_blocking=True)  # the caching host allocator holds `pin` until this copy has run
+        return d
     a = np.ascontiguousarray(a)
     if not a.flags.writeable:  # e.g. a BMAT file's buffer; torch.from_numpy wants a writable array
         a = a.copy()
-    d.copy_(torch().from_numpy(a))
+    d.copy_(t.from_numpy(a))
     return d
 
 
@@ -236,30 +248,33 @@ def _threaded_copy(dst: np.ndarray, src: np.ndarray) -> None:
 
 
 def upload(a: np.ndarray):
-    """to_device for large host matrices: threaded copy into page-locked
-    memory (torch's caching host allocator), then one DMA."""
-    a = np.asarray(a, dtype=np.float64)
-    if a.ndim != 2 or a.nbytes < (16 << 20):
-        return to_device(a)
-    t = torch()
-    d = empty_matrix(a.shape[0], a.shape[1])
-    pin = t.empty(a.shape, dtype=t.float64, pin_memory=True)
-    _threaded_copy(pin.numpy(), a)
-    d.copy_(pin, non_blocking=True)  # the allocator holds `pin` until this copy has run
-    return d
+    """to_device (kept as the name the Schur paths use)."""
+    return to_device(a)
 
 
 def download(d, out: np.ndarray) -> None:
-    """out[...] = d for large matrices: one DMA into page-locked memory, then
-    a threaded copy into the caller's array."""
+    """out[...] = d (device matrix or batch): large results are DMA'd into
+    page-locked memory, then copied into the caller's array by several threads."""
     t = torch()
-    if out.ndim != 2 or out.nbytes < (16 << 20) or out.dtype != np.float64:
+    if out.nbytes < _STAGE_MIN or out.dtype != np.float64 or out.ndim not in (2, 3):
         out[...] = d.cpu().numpy()
         return
     pin = t.empty(tuple(out.shape), dtype=t.float64, pin_memory=True)
     pin.copy_(d, non_blocking=True)
     t.cuda.current_stream().synchronize()
-    _threaded_copy(out, pin.numpy())
+    if out.ndim == 3 and not out[0].flags.c_contiguous:
+        for z in range(out.shape[0]):
+            _threaded_copy(out[z], pin[z].numpy())
+    else:
+        _threaded_copy(out.reshape(-1, out.shape[-1]) if out.flags.c_contiguous else out,
+                       pin.numpy().reshape(-1, out.shape[-1]) if out.flags.c_contiguous else pin.numpy())
+
+
+def to_numpy(d) -> np.ndarray:
+    """A new host array with the values of device matrix (or batch) ``d``."""
+    out = np.empty(tuple(d.shape), dtype=np.float64)
+    download(d, out)
+    return out
 
 
 def workspace(nbytes: int):

@@ -196,7 +196,7 @@ def _mm_acc(a, b, out, negate: bool = False) -> None:
     if out.size and a.shape[1]:
         dout = _lib.to_device(out)
         device_gemm(_lib.to_device(a), _lib.to_device(b), dout, c=dout, negate=negate)
-        out[...] = dout.cpu().numpy()
+        _lib.download(dout, out)
 
 
 def multiply(a, b, out, accumulate=False, negate=False, counters: OpCounters | None = None) -> None:
@@ -214,7 +214,7 @@ def multiply(a, b, out, accumulate=False, negate=False, counters: OpCounters | N
                 out[...] = 0.0
         else:
             device_gemm(da, db, dout, c=dout if accumulate else None, negate=negate)
-            out[...] = dout.cpu().numpy()
+            _lib.download(dout, out)
     if counters is not None:
         counters.multiplies += 1
         if accumulate:
@@ -266,7 +266,7 @@ def _invert_host_block(m: np.ndarray) -> tuple[np.ndarray, int]:
     dm = _lib.to_device(m)
     dout = _lib.empty_matrix(*m.shape)
     info = device_inverse(dm, dout)
-    return dout.cpu().numpy(), int(info[0])
+    return _lib.to_numpy(dout), int(info[0])
 
 
 def invert_small(m, out, counters: OpCounters | None = None) -> None:

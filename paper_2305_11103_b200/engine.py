@@ -217,7 +217,7 @@ def assemble_updown(level: int, minv, t_sets: dict, workers: int = 1,
         device_gemm(_lib.to_device(rb), dm[a1:a2, a1:a2], dm[a0:a1, a1:a2])  # up:   R . M_inv[D, D]
         if counters is not None:
             counters.multiplies += 2
-    out = dm[:, : scheme.m_n].cpu().numpy()
+    out = _lib.to_numpy(dm[:, : scheme.m_n])
     for a0, a1, a2, _, _ in quads:
         store.data[a1:a2, a0:a1] = out[a1:a2, a0:a1]
         store.data[a0:a1, a1:a2] = out[a0:a1, a1:a2]

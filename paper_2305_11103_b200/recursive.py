@@ -177,7 +177,7 @@ def invertor_inplace_by_a(x, row_scratch=None, counters: OpCounters | None = Non
     if n:
         xd = _lib.to_device(x)
         inplace_by_a_device(xd)
-        x[...] = xd.cpu().numpy()
+        _lib.download(xd, x)
     counters.alloc(row_scratch.shape[0])  # recursive.py:289-291
     if n:
         _ref_inplace(n, counters)
@@ -195,7 +195,7 @@ def invertor_by_a(x, counters: OpCounters | None = None):
     if n:
         xd = _lib.to_device(x)
         inplace_by_a_device(xd)
-        out[...] = xd.cpu().numpy()
+        _lib.download(xd, out)
         _ref_by_a(n, counters)
     return out, counters
 
@@ -300,7 +300,7 @@ def invertor_by_ad(x, counters: OpCounters | None = None, parallel_pairs: bool =
         od = _lib.empty_matrix(n, n)
         tree.node(xd, od, 0, [])
         tree.check()
-        out[...] = od.cpu().numpy()
+        _lib.download(od, out)
         _ref_by_ad(n, 0, set(), counters)
     return out, counters
 
@@ -328,7 +328,7 @@ def invertor_with_fallback(x, counters: OpCounters | None = None):
         do = _lib.empty_matrix(*dm.shape)
         if int(device_inverse(dm, do)[0]):
             raise SingularBlock("A", path=[])
-        out[...] = do.cpu().numpy()
+        _lib.download(do, out)
         counters.inversions += 1
 
     def sub(block, out):
