@@ -578,6 +578,16 @@ def run_sharded_arm(args) -> None:
             "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
             "residual_fro": float(fro),
         }
+        # K1's algorithmic flops per GPU (arrows 2n^3 - 2n^2 b, up/down n^3 - n^2 b) over the WHOLE
+        # sharded step -- leaf steps and exchanges included, so a lower bound of the kernel's own rate
+        b = N // NBLOCKS
+        gemm_flops = 3.0 * N**3 - 3.0 * N**2 * b
+        ach = gemm_flops / world / (ms_step * 1e-3) / 1e12
+        line["roofline"] = {"bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": UNIT,
+                            "frac": ach / FP64_PEAK_TFLOPS, "traffic": None, "peak_source": FP64_PEAK_SOURCE,
+                            "kernel": "gemm_tma_refill_kernel (K1, engine GEMM ops), per GPU",
+                            "note": "per-GPU algorithmic GEMM flops over the whole sharded step (leaves and "
+                                    "exchanges included): a lower bound of the kernel's own rate"}
         if share:
             line["harness_self_test"] = "BI_BENCH_SHARE_GPU=1: ranks share one GPU over gloo -- not a measurement"
         print(json.dumps(line), flush=True)
