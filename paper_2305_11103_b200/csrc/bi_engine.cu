@@ -563,21 +563,26 @@ static int build_schedule(bi_engine* e) {
       x.bot_rows = hd;
       x.rows = ha + hd;
     } else {  // up/down pass: A-half ranks share their L columns, D-half ranks their R columns
+      // The exchange stays inside the rank's own half of the group: only those
+      // ranks read its part, and only they send parts of the same height (L is
+      // hd x ha, R is ha x hd: with ragged block orders the halves differ, and
+      // an all-gather needs equal contributions).  A half of one rank
+      // (gs == 1) is a local copy.
       if (x.in_a) {
         part(e->tset_window(lv, 0, mid, last, e->h0, e->h1), x.top, x.top_ld);
         x.top_rows = hd;
-        x.from0 = x.g0;
-        x.from1 = x.g0 + half;
         x.x_col0 = off[first];
         x.xcols = ha;
       } else {
         part(e->tset_window(lv, 0, first, mid, e->h0, e->h1), x.top, x.top_ld);
         x.top_rows = ha;
-        x.from0 = x.g0 + half;
-        x.from1 = x.g0 + x.gs;
+        x.g0 += half;
         x.x_col0 = off[mid];
         x.xcols = hd;
       }
+      x.gs = half;
+      x.from0 = x.g0;
+      x.from1 = x.g0 + x.gs;
       x.rows = x.top_rows;
     }
     x.ldx = round_up(x.xcols, 4);
@@ -2149,10 +2154,12 @@ extern "C" int bi_engine_xchg_pack(bi_engine* e, int i, void* stream) {
   BI_REQUIRE(e->send_elems > 0, "engine created without BI_SHARD_STAGING");
   const auto& x = e->xchgs[i];
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  BI_CUDA_TRY(cudaMemcpy2DAsync(e->sendbuf, e->wmax * 8, x.top, x.top_ld * 8, e->w * 8, x.top_rows,
+  // a group of one rank has no collective: pack straight into the receive area
+  double* dst = x.gs == 1 ? e->recvbuf : e->sendbuf;
+  BI_CUDA_TRY(cudaMemcpy2DAsync(dst, e->wmax * 8, x.top, x.top_ld * 8, e->w * 8, x.top_rows,
                                 cudaMemcpyDeviceToDevice, s));
   if (x.bot)
-    BI_CUDA_TRY(cudaMemcpy2DAsync(e->sendbuf + x.top_rows * e->wmax, e->wmax * 8, x.bot, x.bot_ld * 8, e->w * 8,
+    BI_CUDA_TRY(cudaMemcpy2DAsync(dst + x.top_rows * e->wmax, e->wmax * 8, x.bot, x.bot_ld * 8, e->w * 8,
                                   x.bot_rows, cudaMemcpyDeviceToDevice, s));
   return 0;
 }

@@ -154,13 +154,15 @@ extern "C" int bi_engine_run_nccl(bi_engine* e, int first_step, int last_step, i
     int64_t d[8];
     bi_engine_xchg_desc(e, x[k], d);
     const int gs = (int)d[1];
-    auto it = comms.find(gs);
-    BI_REQUIRE(it != comms.end(), "group communicators missing: call bi_engine_shard_set_comm first");
     if ((rc = bi_engine_xchg_pack(e, x[k], stream)) != 0) return rc;
-    double *send = nullptr, *recv = nullptr;
-    bi_engine_shard_buffers(e, &send, &recv);
-    BI_NCCL_TRY(nccl().AllGather(send, recv, (size_t)(d[2] * d[3]), ncclDouble,
-                                 static_cast<ncclComm_t>(it->second), s));
+    if (gs > 1) {  // (a group of one packs straight into the receive area)
+      auto it = comms.find(gs);
+      BI_REQUIRE(it != comms.end(), "group communicators missing: call bi_engine_shard_set_comm first");
+      double *send = nullptr, *recv = nullptr;
+      bi_engine_shard_buffers(e, &send, &recv);
+      BI_NCCL_TRY(nccl().AllGather(send, recv, (size_t)(d[2] * d[3]), ncclDouble,
+                                   static_cast<ncclComm_t>(it->second), s));
+    }
     if ((rc = bi_engine_xchg_unpack(e, x[k], stream)) != 0) return rc;
   }
   return 0;

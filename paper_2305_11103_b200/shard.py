@@ -154,6 +154,9 @@ class NativeShard:
             x = self._x[xi]
             chunk = x["rows"] * self.wmax
             _lib.check(L.bi_engine_xchg_pack(self._h, xi, st), "bi_engine_xchg_pack")
+            if x["gs"] == 1:  # an up/down half of one rank: packed straight into the receive area
+                _lib.check(L.bi_engine_xchg_unpack(self._h, xi, st), "bi_engine_xchg_unpack")
+                continue
             send = self._flat[self._send_off:self._send_off + chunk]
             recv = self._flat[self._recv_off:self._recv_off + x["gs"] * chunk]
             pg = groups[(x["gs"], x["g0"])]

@@ -96,7 +96,8 @@ def test_run_inversion_workers_takes_native_group(bi, monkeypatch):
 
 def test_plan_matches_python_scheduler(bi):
     """The native exchange plan equals the host scheduler's (distributed.py):
-    one exchange per global-level action, groups of 2^l / (N_b/P) ranks."""
+    one exchange per global-level action, groups of 2^l / (N_b/P) ranks (arrows)
+    or the rank's own half of them (up/down passes)."""
     from paper_2305_11103_b200.engine import decode_step, loopid_for_step, total_steps
     from paper_2305_11103_b200.shard import NativeShard
 
@@ -116,9 +117,13 @@ def test_plan_matches_python_scheduler(bi):
         got = [(x["kind"], x["level"]) for x in sh._x]
         assert got == expect
         for x in sh._x:
-            gs = (1 << x["level"]) // nbp
-            assert x["gs"] == gs and x["g0"] == r // gs * gs
-            assert x["in_a"] == (r - x["g0"] < gs // 2)
+            gs = (1 << x["level"]) // nbp  # the quad's ranks; an up/down pass exchanges inside its own half
+            in_a = r - r // gs * gs < gs // 2
+            assert x["in_a"] == in_a
+            if x["kind"] == "updown":
+                assert x["gs"] == gs // 2 and x["g0"] == r // (gs // 2) * (gs // 2)
+            else:
+                assert x["gs"] == gs and x["g0"] == r // gs * gs
 
 
 def test_library_nccl_transport_single_rank(bi):
