@@ -207,7 +207,11 @@ int bi_engine_status(bi_engine* e, int* fail_step, int* fail_quad, int* fail_mat
  *   Transport B, one process per GPU: create with BI_SHARD_STAGING, then per
  *   exchange bi_engine_xchg_pack (send parts -> send area, rows x wmax),
  *   an all-gather of the send areas inside the group (NCCL) into the receive
- *   area ([gs][rows][wmax]), bi_engine_xchg_unpack (-> X).
+ *   area ([gs][rows][wmax]), bi_engine_xchg_unpack (-> X).  The group
+ *   [g0, g0 + gs) of bi_engine_xchg_desc is the quad's ranks for an arrows
+ *   exchange and the rank's own half of them for an up/down pass (equal part
+ *   heights inside a half, also with ragged block orders); gs == 1 packs
+ *   straight into the receive area and needs no collective.
  * ---------------------------------------------------------------------- */
 #define BI_SHARD_STAGING 1
 int bi_engine_create_shard(bi_engine** out, int nblocks, const int64_t* sizes, int nranks, int rank, int flags);
