@@ -1,5 +1,6 @@
 """GPU: the opt-in tuning knobs (DESIGN 8) keep results correct.  Each knob is
-read once per process, so every combination runs in a fresh interpreter:
+read once per process, so every combination runs in a fresh interpreter
+(six interpreters at a time):
 K3 alone (n = 300 / 512 / 1000) and the engine (8 x 64 and 4 x 128 blocks)
 against the oracle, relF <= 1e-12 / 1e-9."""
 
@@ -62,11 +63,31 @@ KNOBS = [
 ]
 
 
-@pytest.mark.parametrize("knobs", KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()))
-def test_knob_combination_correct(knobs):
-    env = dict(os.environ, **knobs)
-    r = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT)], env=env, capture_output=True, text=True,
-                       timeout=600)
+def _knob_id(k: dict) -> str:
+    return ",".join(f"{a}={b}" for a, b in k.items())
+
+
+@pytest.fixture(scope="module")
+def knob_runs():
+    """Every combination's interpreter, six at a time (most of a run is the
+    interpreter start and the CPU oracle, not the GPU): the per-knob tests
+    below only collect their own result."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(knobs):
+        env = dict(os.environ, **knobs)
+        return subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT)], env=env, capture_output=True, text=True,
+                              timeout=600)
+
+    pool = ThreadPoolExecutor(max_workers=6)
+    futures = {_knob_id(k): pool.submit(run, k) for k in KNOBS}
+    yield futures
+    pool.shutdown(wait=False, cancel_futures=True)
+
+
+@pytest.mark.parametrize("knobs", KNOBS, ids=_knob_id)
+def test_knob_combination_correct(knobs, knob_runs):
+    r = knob_runs[_knob_id(knobs)].result(timeout=1200)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
 
 
